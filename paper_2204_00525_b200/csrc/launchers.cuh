@@ -1,0 +1,139 @@
+// Host-side launchers of the device kernels (one per kernel family).
+#pragma once
+
+#include "fg_internal.cuh"
+
+namespace fg {
+
+constexpr int kMaxKeyCols = 16;
+constexpr int kMaxChildren = 16;
+
+// Field layout of a packed key: field f takes `bits[f]` bits at `shift[f]`
+// and encodes the attribute value v as (u64)(v - min[f]).
+struct PackSpec {
+  int n;
+  int col[kMaxKeyCols];  // source key column (pack) / source field (project)
+  int shift[kMaxKeyCols];
+  int bits[kMaxKeyCols];
+  long long min[kMaxKeyCols];
+};
+
+// ---- group.cu -------------------------------------------------------------
+// Per key column min/max over rows (atomics into mins/maxs[attr_of_col]).
+void launch_key_minmax(Context& ctx, const int64_t* keys, int64_t rows,
+                       int n_key, const int* attr_of_col_dev,
+                       long long* mins, long long* maxs);
+// Packs int64 key tuples into u64 keys (declaration order, MSB first) and
+// writes the identity permutation.
+void launch_pack_keys(Context& ctx, const int64_t* keys, int64_t rows,
+                      int n_key, const PackSpec& spec, uint64_t* out,
+                      int* iota);
+// Re-packs already packed keys into another field layout (projection).
+void launch_project(Context& ctx, const uint64_t* in, int64_t n,
+                    const PackSpec& from_to, uint64_t* out);
+// Stable radix sort of (key, perm) on the low `bits` bits + run-length
+// grouping.  perm_in is overwritten.  Returns G (host; synchronises).
+struct GroupOut {
+  DevArray<int> perm;       // n
+  DevArray<int> begins;     // G + 1
+  DevArray<uint64_t> uniq;  // G
+  DevArray<uint64_t> sorted;  // n (only with keep_sorted)
+  int64_t G = 0;
+};
+void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
+                  const int* perm_in, GroupOut& out, bool keep_sorted = false);
+// Without syncing: sort only (keys_out/perm_out) -- used when the caller
+// batches syncs itself.
+void sort_pairs(Context& ctx, const uint64_t* keys_in, uint64_t* keys_out,
+                const int* vals_in, int* vals_out, int64_t n, int bits);
+// Run-length encode a sorted key array. Writes uniq, counts and *num_runs
+// (device); no sync.
+void run_length(Context& ctx, const uint64_t* sorted, int64_t n,
+                uint64_t* uniq, int* counts, int64_t* num_runs_dev);
+void exclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
+void inclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
+// pidx[perm[s]] = run id of sorted position s.
+void launch_run_ids(Context& ctx, const uint64_t* sorted, const int* perm,
+                    int64_t n, int* scratch_flags, int* scratch_scan,
+                    int* pidx);
+// For each of n packed keys (projected to the child's parent-key layout by
+// `proj`), binary search it in sorted `table` (size m); write the index or
+// flag ST_MISSING_CHILD and write -1.
+void launch_lookup(Context& ctx, const uint64_t* own_keys, int64_t n,
+                   const PackSpec& proj, const uint64_t* table, int64_t m,
+                   int* out, unsigned* status);
+// Decodes packed keys back to int64 tuples (n x spec.n).
+void launch_unpack(Context& ctx, const uint64_t* in, int64_t n,
+                   const PackSpec& spec, int64_t* out);
+void launch_iota(Context& ctx, int* out, int64_t n);
+// counts[g] = begins[g+1] - begins[g]
+void launch_seg_sizes(Context& ctx, const int* begins, int64_t G,
+                      uint64_t* sizes);
+
+// ---- counts.cu ------------------------------------------------------------
+struct ChildLinks {
+  int n;
+  const int* lidx[kMaxChildren];       // own segment -> child parent-key idx
+  uint64_t* phi_down[kMaxChildren];
+  uint64_t* phi_up[kMaxChildren];
+};
+void launch_theta(Context& ctx, const uint64_t* sizes, int64_t G,
+                  const ChildLinks& ch, const int* pidx, uint64_t* phi_down,
+                  uint64_t* theta, unsigned* status);
+void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
+                int64_t G, const int* pidx, const uint64_t* phi_up,
+                const ChildLinks& ch, uint64_t* fjs, uint64_t* circ,
+                unsigned* status);
+void launch_up_div(Context& ctx, uint64_t* phi_up, const uint64_t* phi_down,
+                   int64_t P, unsigned* status);
+
+// ---- headtail.cu ----------------------------------------------------------
+struct HeadTailArgs {
+  const double* data = nullptr;
+  int64_t ld = 0;
+  int w = 0;
+  const int* perm = nullptr;        // sorted pos -> source row (null = id)
+  const int* begins = nullptr;      // G + 1
+  int64_t n_seg = 0;
+  int64_t n_rows = 0;               // begins[G]
+  const double* weights = nullptr;  // per source row (generalized mode)
+  const uint64_t* tail_count = nullptr;   // tails *= sqrt(tail_count[g])
+  const uint64_t* scale_count = nullptr;  // scale = sqrt(scale_count[g])
+  const int* head_index = nullptr;  // output row of head/scale (null = g)
+  double* heads = nullptr;
+  int64_t ldh = 0;
+  double* tails = nullptr;
+  int64_t ldt = 0;
+  double* scales = nullptr;
+};
+// Runs the segmented (generalized) head/tail transform.  Needs the max
+// segment size only to decide whether the heavy-segment pre-pass runs.
+void run_heads_tails(Context& ctx, const HeadTailArgs& a);
+
+struct JoinArgs {
+  int64_t G = 0;
+  int own_w = 0;
+  double* S = nullptr;  // G x width, own head in [0, own_w)
+  int64_t width = 0;
+  double* scale = nullptr;  // G
+  int n_children = 0;
+  const int* lidx[kMaxChildren];
+  const double* child_S[kMaxChildren];
+  const double* child_scale[kMaxChildren];
+  int child_w[kMaxChildren];
+  int child_off[kMaxChildren];  // local column offset in S
+};
+void launch_join(Context& ctx, const JoinArgs& a);
+
+// ---- tsqr.cu ----------------------------------------------------------------
+struct Span {
+  const double* data;
+  int64_t rows;
+  int64_t ld;
+  int cols;
+  int col_begin;
+};
+// R (n x n, row-major, device) of the stacked spans, sign-normalised.
+void tsqr(Context& ctx, const std::vector<Span>& spans, int n, double* R_out);
+
+}  // namespace fg

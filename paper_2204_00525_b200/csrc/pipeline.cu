@@ -1,0 +1,1105 @@
+// Host orchestration of the device pipeline and the C ABI (figaro_cuda.h).
+//
+// fg_run_pipeline restates figaro::run_pipeline (driver.hpp:47-85):
+//   validate_join_tree + build_join_tree   -> host (join_tree.hpp:72-180)
+//   semi_join_reduce (unless assume_reduced) -> device selection vectors
+//                                               (reduce.hpp:47-74)
+//   make_layout                            -> host (join_tree.hpp:186-219)
+//   canonical grouping                     -> K1 (group.cu)
+//   compute_counts                         -> K2 (counts.cu)
+//   figaro_r0                              -> K3/K4/K5 (headtail.cu)
+//   postprocess_thin + normalize_signs     -> K6/K7 (tsqr.cu)
+// Device phases are timed with CUDA events on the context stream.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "launchers.cuh"
+
+namespace fg {
+
+struct NodeState {
+  std::string name;
+  int n_key = 0, w = 0;
+  int64_t rows_in = 0;   // rows as passed in
+  int64_t rows = 0;      // rows after reduction
+  std::vector<std::string> key_names, data_names;
+  std::vector<int> key_attr;    // global attribute ids, declaration order
+  std::vector<int> pattr;       // parent-shared attribute ids, name order
+  std::vector<std::string> pattr_names;
+  int parent = -1;
+  std::vector<int> children;
+  const int64_t* keys = nullptr;
+  const double* data = nullptr;
+  DevArray<int64_t> keys_own;
+  DevArray<double> data_own;
+  DevArray<int> sel;            // selected rows after reduction (or empty)
+  bool has_sel = false;
+  PackSpec own{};               // int64 key columns -> packed own key
+  int own_bits = 0;
+  GroupOut grp;
+  DevArray<uint64_t> sizes;
+  // parent-key grouping of own segments
+  DevArray<int> pa_perm, pa_begins, pidx;
+  DevArray<uint64_t> upk;
+  int64_t P = 0;
+  PackSpec par{};               // own packed -> parent key (pattr order)
+  std::vector<DevArray<int>> lidx;  // per child
+  DevArray<uint64_t> theta, fjs, circ, phi_down, phi_up;
+  // summaries
+  int64_t width = 0;
+  DevArray<double> S, scale, Sq, scale_q;
+  const double* sum_S = nullptr;
+  const double* sum_scale = nullptr;
+  DevArray<double> tails, ptails;
+};
+
+struct SpanInfo {
+  int node;
+  int64_t col_begin;
+  int64_t rows;
+  int64_t cols;
+  const double* data;
+};
+
+struct Context::Saved {
+  std::vector<std::unique_ptr<NodeState>> nodes;
+  std::vector<SpanInfo> spans;
+  bool have_r0 = false;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- host tree
+
+void build_tree(std::vector<std::unique_ptr<NodeState>>& nodes, int root,
+                const int32_t* parent, std::vector<int>& preorder) {
+  const int r = (int)nodes.size();
+  if (r == 0) fail(FG_E_TREE, "join tree: no relations");
+  if (root < 0 || root >= r) fail(FG_E_TREE, "join tree: bad root index");
+  for (int i = 0; i < r; ++i) {
+    const int p = parent[i];
+    nodes[i]->parent = p;
+    if (i == root) {
+      if (p != -1) fail(FG_E_TREE, "join tree: root cannot have a parent");
+      continue;
+    }
+    if (p < 0 || p >= r)
+      fail(FG_E_TREE, "join tree: bad parent index for node " + nodes[i]->name);
+    nodes[p]->children.push_back(i);
+    // parent_attrs: shared key attributes sorted by name (join_tree.hpp:37-45)
+    std::set<std::string> pk(nodes[p]->key_names.begin(),
+                             nodes[p]->key_names.end());
+    std::vector<std::string> shared;
+    for (const auto& k : nodes[i]->key_names)
+      if (pk.count(k)) shared.push_back(k);
+    std::sort(shared.begin(), shared.end());
+    nodes[i]->pattr_names = shared;
+  }
+  std::vector<int> stack{root};
+  std::vector<char> seen(r, 0);
+  // Pre-order, children in index order (join_tree.hpp:47-51).
+  std::function<void(int)> walk = [&](int n) {
+    if (seen[n]) fail(FG_E_TREE, "join tree: not a connected tree");
+    seen[n] = 1;
+    preorder.push_back(n);
+    for (int c : nodes[n]->children) walk(c);
+  };
+  walk(root);
+  if ((int)preorder.size() != r)
+    fail(FG_E_TREE, "join tree: not a connected tree");
+}
+
+// join_tree.hpp:104-180 (path property, every key attribute shared, data
+// attribute names disjoint from everything else) + canonicalize's schema
+// checks (relation.hpp:128-146).
+void validate(const std::vector<std::unique_ptr<NodeState>>& nodes) {
+  for (const auto& n : nodes) {
+    std::vector<std::string> names = n->key_names;
+    names.insert(names.end(), n->data_names.begin(), n->data_names.end());
+    std::sort(names.begin(), names.end());
+    auto dup = std::adjacent_find(names.begin(), names.end());
+    if (dup != names.end())
+      fail(FG_E_SCHEMA, "relation " + n->name + ": duplicate attribute '" +
+                            *dup + "'");
+    for (const auto& s : names)
+      if (s.empty())
+        fail(FG_E_SCHEMA, "relation " + n->name + ": empty attribute name");
+  }
+  const int r = (int)nodes.size();
+  if (r <= 1) return;
+  auto path_between = [&](int a, int b) {
+    std::vector<int> up_a, up_b;
+    for (int x = a; x != -1; x = nodes[x]->parent) up_a.push_back(x);
+    for (int x = b; x != -1; x = nodes[x]->parent) up_b.push_back(x);
+    std::set<int> anc(up_a.begin(), up_a.end());
+    int meet = -1;
+    for (int x : up_b)
+      if (anc.count(x)) { meet = x; break; }
+    std::vector<int> path;
+    for (int x : up_a) { path.push_back(x); if (x == meet) break; }
+    std::vector<int> down;
+    for (int x : up_b) { if (x == meet) break; down.push_back(x); }
+    path.insert(path.end(), down.rbegin(), down.rend());
+    return path;
+  };
+  std::map<std::string, std::vector<int>> attr_nodes;
+  for (int i = 0; i < r; ++i)
+    for (const auto& a : nodes[i]->key_names) attr_nodes[a].push_back(i);
+  for (const auto& [attr, ns] : attr_nodes) {
+    if (ns.size() < 2)
+      fail(FG_E_TREE, "key attribute '" + attr + "' of relation " +
+                          nodes[ns[0]]->name +
+                          " is not shared with any other relation");
+    for (size_t x = 0; x < ns.size(); ++x)
+      for (size_t y = x + 1; y < ns.size(); ++y)
+        for (int n : path_between(ns[x], ns[y])) {
+          const auto& ks = nodes[n]->key_names;
+          if (std::find(ks.begin(), ks.end(), attr) == ks.end())
+            fail(FG_E_TREE, "path property violated for attribute '" + attr +
+                                "': relation " + nodes[n]->name +
+                                " does not contain it");
+        }
+  }
+  std::map<std::string, int> data_owner;
+  for (int i = 0; i < r; ++i)
+    for (const auto& a : nodes[i]->data_names) {
+      auto [it, fresh] = data_owner.emplace(a, i);
+      if (!fresh)
+        fail(FG_E_SCHEMA, "data attribute '" + a + "' appears in both " +
+                              nodes[it->second]->name + " and " +
+                              nodes[i]->name);
+      if (attr_nodes.count(a))
+        fail(FG_E_SCHEMA, "attribute '" + a + "' is a data column of " +
+                              nodes[i]->name + " but a key column elsewhere");
+    }
+}
+
+struct Layout {
+  int64_t total = 0;
+  std::vector<int64_t> node_offset, node_width, sub_begin, sub_end;
+};
+
+Layout make_layout(const std::vector<std::unique_ptr<NodeState>>& nodes,
+                   const std::vector<int>& preorder, int root) {
+  Layout l;
+  const size_t r = nodes.size();
+  l.node_offset.resize(r);
+  l.node_width.resize(r);
+  l.sub_begin.resize(r);
+  l.sub_end.resize(r);
+  for (int n : preorder) {
+    l.node_offset[n] = l.total;
+    l.node_width[n] = nodes[n]->w;
+    l.total += nodes[n]->w;
+  }
+  std::function<int64_t(int)> fill = [&](int n) -> int64_t {
+    l.sub_begin[n] = l.node_offset[n];
+    int64_t end = l.node_offset[n] + l.node_width[n];
+    for (int c : nodes[n]->children) end = fill(c);
+    l.sub_end[n] = end;
+    return end;
+  };
+  fill(root);
+  return l;
+}
+
+// ---------------------------------------------------------------- encoding
+
+struct AttrCode {
+  long long min = 0;
+  int bits = 0;
+};
+
+int bitlen(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+// Fields of `attrs` (attribute ids, in this order) packed MSB first, taking
+// values from source positions given by `src(attr)`.
+PackSpec make_spec(const std::vector<int>& attrs,
+                   const std::vector<AttrCode>& code,
+                   const std::function<int(int)>& src, int* total_bits,
+                   const std::string& what) {
+  PackSpec s{};
+  if (attrs.size() > (size_t)kMaxKeyCols)
+    fail(FG_E_UNSUPPORTED, what + ": more than 16 key attributes");
+  s.n = (int)attrs.size();
+  int total = 0;
+  for (int a : attrs) total += code[a].bits;
+  if (total > 64)
+    fail(FG_E_UNSUPPORTED, what + ": key tuple needs " + std::to_string(total) +
+                               " bits after range packing (> 64)");
+  int pos = total;
+  for (int f = 0; f < s.n; ++f) {
+    const int a = attrs[f];
+    pos -= code[a].bits;
+    s.shift[f] = pos;
+    s.bits[f] = code[a].bits;
+    s.min[f] = code[a].min;
+    s.col[f] = src(a);
+  }
+  if (total_bits) *total_bits = total;
+  return s;
+}
+
+// --------------------------------------------------------------- reduction
+
+__global__ void k_pack_sel(const int64_t* __restrict__ keys, int n_key,
+                           const int* __restrict__ sel, int64_t n,
+                           PackSpec spec, uint64_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = sel ? sel[t] : t;
+    uint64_t k = 0;
+    for (int f = 0; f < spec.n; ++f) {
+      const long long v = keys[i * n_key + spec.col[f]];
+      if (spec.bits[f]) k |= ((uint64_t)v - (uint64_t)spec.min[f]) << spec.shift[f];
+    }
+    out[t] = k;
+  }
+}
+
+__global__ void k_member(const uint64_t* __restrict__ q, int64_t n,
+                         const uint64_t* __restrict__ table, int64_t m,
+                         char* __restrict__ keep) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = q[t];
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (table[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    keep[t] = (lo < m && table[lo] == key) ? 1 : 0;
+  }
+}
+
+int grid1d(const Context& ctx, int64_t n) {
+  int64_t g = ceil_div(n, 256);
+  const int64_t cap = (int64_t)ctx.sm_count * 8;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+// Packs the projection of node `i`'s selected rows onto `attrs`.
+void pack_projection(Context& ctx, NodeState& n, const std::vector<int>& attrs,
+                     const std::vector<AttrCode>& code, DevArray<uint64_t>& out) {
+  PackSpec s = make_spec(attrs, code,
+                         [&](int a) {
+                           return (int)(std::find(n.key_attr.begin(),
+                                                  n.key_attr.end(), a) -
+                                        n.key_attr.begin());
+                         },
+                         nullptr, "semi-join");
+  out.alloc(n.rows, ctx.stream);
+  if (n.rows == 0) return;
+  k_pack_sel<<<grid1d(ctx, n.rows), 256, 0, ctx.stream>>>(
+      n.keys, n.n_key, n.has_sel ? n.sel.get() : nullptr, n.rows, s,
+      out.get());
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
+}
+
+// semi_join (reduce.hpp:20-43): keep rows of `a` whose projection onto
+// `attrs` occurs in `b`.  Row order is preserved (selection vector).
+void semi_join(Context& ctx, NodeState& a, NodeState& b,
+               const std::vector<int>& attrs, const std::vector<AttrCode>& code) {
+  if (attrs.empty()) return;
+  DevArray<uint64_t> qa, qb;
+  pack_projection(ctx, a, attrs, code, qa);
+  pack_projection(ctx, b, attrs, code, qb);
+  DevArray<uint64_t> tb(b.rows, ctx.stream);
+  if (b.rows) {
+    int bits = 0;
+    for (int x : attrs) bits += code[x].bits;
+    size_t temp = 0;
+    FG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, qb.get(), tb.get(),
+                                           b.rows, 0, std::max(bits, 1),
+                                           ctx.stream));
+    DevArray<unsigned char> tmp(temp, ctx.stream);
+    FG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), temp, qb.get(), tb.get(),
+                                           b.rows, 0, std::max(bits, 1),
+                                           ctx.stream));
+    ctx.launches += 3;
+  }
+  DevArray<char> keep(a.rows, ctx.stream);
+  if (a.rows) {
+    k_member<<<grid1d(ctx, a.rows), 256, 0, ctx.stream>>>(
+        qa.get(), a.rows, tb.get(), b.rows, keep.get());
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+  }
+  DevArray<int> cur;
+  if (!a.has_sel) {
+    cur.alloc(a.rows, ctx.stream);
+    launch_iota(ctx, cur.get(), a.rows);
+  } else {
+    cur = std::move(a.sel);
+  }
+  DevArray<int> next(a.rows, ctx.stream);
+  DevArray<int64_t> nsel(1, ctx.stream);
+  size_t temp = 0;
+  FG_CUDA(cub::DeviceSelect::Flagged(nullptr, temp, cur.get(), keep.get(),
+                                     next.get(), nsel.get(), a.rows,
+                                     ctx.stream));
+  DevArray<unsigned char> tmp(temp, ctx.stream);
+  FG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), temp, cur.get(), keep.get(),
+                                     next.get(), nsel.get(), a.rows,
+                                     ctx.stream));
+  ctx.launches += 2;
+  int64_t m = 0;
+  FG_CUDA(cudaMemcpyAsync(&m, nsel.get(), sizeof m, cudaMemcpyDeviceToHost,
+                          ctx.stream));
+  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  a.sel = std::move(next);
+  a.has_sel = true;
+  a.rows = m;
+}
+
+void check_nonempty(const NodeState& n) {
+  if (n.rows == 0)
+    fail(FG_E_EMPTY_JOIN, "relation " + n.name +
+                              " reduced to empty: the join result is empty");
+}
+
+// --------------------------------------------------------------- status
+
+void check_status(Context& ctx, const char* phase) {
+  unsigned st = 0;
+  FG_CUDA(cudaMemcpyAsync(&st, ctx.status.get(), sizeof st,
+                          cudaMemcpyDeviceToHost, ctx.stream));
+  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (!st) return;
+  const std::string p = phase;
+  if (st & ST_MISSING_CHILD)
+    fail(FG_E_INTEGRITY, p + ": a key has no match in a child relation; is the "
+                             "database fully reduced?");
+  if (st & ST_OVERFLOW)
+    fail(FG_E_SIZE, "count aggregate overflow (64-bit)");
+  if (st & ST_UP_UNMATCHED)
+    fail(FG_E_INTEGRITY, p + ": a child has keys unmatched in its parent; is "
+                             "the database fully reduced?");
+  if (st & ST_CIRC_INEXACT)
+    fail(FG_E_INTEGRITY, p + ": phi_circ: counts are inconsistent; is the "
+                             "database fully reduced?");
+  if (st & ST_UP_INEXACT)
+    fail(FG_E_INTEGRITY, p + ": phi_up: counts are inconsistent; is the "
+                             "database fully reduced?");
+  fail(FG_E_INTEGRITY, p + ": inconsistent counts");
+}
+
+struct Events {
+  cudaEvent_t e[6];
+  Events() { for (auto& x : e) cudaEventCreate(&x); }
+  ~Events() { for (auto& x : e) cudaEventDestroy(x); }
+  double ms(int a, int b) {
+    float t = 0;
+    cudaEventElapsedTime(&t, e[a], e[b]);
+    return t * 1e-3;
+  }
+};
+
+// ---------------------------------------------------------------- pipeline
+
+void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
+         const int32_t* parent, const fg_options& opt, double* R_out,
+         fg_result* res) {
+  if (n_rel <= 0 || !rels || !parent) fail(FG_E_ARG, "no relations");
+  cudaStream_t st = ctx.stream;
+  const int64_t launches0 = ctx.launches;
+  auto saved = std::make_unique<Context::Saved>();
+  auto& nodes = saved->nodes;
+  for (int i = 0; i < n_rel; ++i) {
+    const fg_relation& r = rels[i];
+    auto n = std::make_unique<NodeState>();
+    n->name = r.name ? r.name : ("R" + std::to_string(i));
+    n->n_key = r.n_key;
+    n->w = r.n_data;
+    n->rows_in = n->rows = r.rows;
+    if (r.n_key < 0 || r.n_data < 0 || r.rows < 0)
+      fail(FG_E_ARG, "relation " + n->name + ": negative size");
+    if (r.rows > INT_MAX)
+      fail(FG_E_UNSUPPORTED, "relation " + n->name + ": more than 2^31-1 rows");
+    if ((r.rows && r.n_key && !r.keys) || (r.rows && r.n_data && !r.data))
+      fail(FG_E_ARG, "relation " + n->name + ": null keys/data");
+    for (int k = 0; k < r.n_key; ++k)
+      n->key_names.push_back(r.key_attrs && r.key_attrs[k] ? r.key_attrs[k] : "");
+    for (int k = 0; k < r.n_data; ++k)
+      n->data_names.push_back(r.data_attrs && r.data_attrs[k] ? r.data_attrs[k]
+                                                              : "");
+    nodes.push_back(std::move(n));
+  }
+  std::vector<int> preorder;
+  build_tree(nodes, root, parent, preorder);
+  validate(nodes);
+  const Layout lay = make_layout(nodes, preorder, root);
+  if (lay.total > 128)
+    fail(FG_E_UNSUPPORTED, "more than 128 data columns in total");
+
+  Events ev;
+  FG_CUDA(cudaEventRecord(ev.e[0], st));
+
+  // Inputs on the device.
+  for (int i = 0; i < n_rel; ++i) {
+    NodeState& n = *nodes[i];
+    const fg_relation& r = rels[i];
+    if (opt.memory == FG_MEM_HOST) {
+      n.keys_own.alloc(r.rows * r.n_key, st);
+      n.data_own.alloc(r.rows * r.n_data, st);
+      if (n.keys_own.size())
+        FG_CUDA(cudaMemcpyAsync(n.keys_own.get(), r.keys, n.keys_own.bytes(),
+                                cudaMemcpyHostToDevice, st));
+      if (n.data_own.size())
+        FG_CUDA(cudaMemcpyAsync(n.data_own.get(), r.data, n.data_own.bytes(),
+                                cudaMemcpyHostToDevice, st));
+      n.keys = n.keys_own.get();
+      n.data = n.data_own.get();
+    } else {
+      n.keys = r.keys;
+      n.data = r.data;
+    }
+  }
+  FG_CUDA(cudaEventRecord(ev.e[1], st));
+  ctx.status.zero();
+
+  // ---- attribute encodings (global, per attribute name)
+  std::map<std::string, int> attr_id;
+  for (auto& n : nodes)
+    for (const auto& k : n->key_names) {
+      auto it = attr_id.emplace(k, (int)attr_id.size()).first;
+      n->key_attr.push_back(it->second);
+    }
+  for (auto& n : nodes)
+    for (const auto& k : n->pattr_names) n->pattr.push_back(attr_id.at(k));
+  const int n_attr = (int)attr_id.size();
+  std::vector<AttrCode> code(n_attr);
+  if (n_attr) {
+    std::vector<long long> init_min(n_attr, LLONG_MAX), init_max(n_attr, LLONG_MIN);
+    DevArray<long long> dmin(n_attr, st), dmax(n_attr, st);
+    FG_CUDA(cudaMemcpyAsync(dmin.get(), init_min.data(), dmin.bytes(),
+                            cudaMemcpyHostToDevice, st));
+    FG_CUDA(cudaMemcpyAsync(dmax.get(), init_max.data(), dmax.bytes(),
+                            cudaMemcpyHostToDevice, st));
+    std::vector<DevArray<int>> col_attr;
+    for (auto& n : nodes) {
+      DevArray<int> ca(n->n_key, st);
+      if (n->n_key)
+        FG_CUDA(cudaMemcpyAsync(ca.get(), n->key_attr.data(), ca.bytes(),
+                                cudaMemcpyHostToDevice, st));
+      launch_key_minmax(ctx, n->keys, n->rows, n->n_key, ca.get(), dmin.get(),
+                        dmax.get());
+      col_attr.push_back(std::move(ca));
+    }
+    std::vector<long long> hmin(n_attr), hmax(n_attr);
+    FG_CUDA(cudaMemcpyAsync(hmin.data(), dmin.get(), dmin.bytes(),
+                            cudaMemcpyDeviceToHost, st));
+    FG_CUDA(cudaMemcpyAsync(hmax.data(), dmax.get(), dmax.bytes(),
+                            cudaMemcpyDeviceToHost, st));
+    FG_CUDA(cudaStreamSynchronize(st));
+    for (int a = 0; a < n_attr; ++a) {
+      if (hmin[a] > hmax[a]) { code[a] = {0, 0}; continue; }  // no rows
+      code[a].min = hmin[a];
+      code[a].bits = bitlen((uint64_t)hmax[a] - (uint64_t)hmin[a]);
+    }
+  }
+
+  // ---- semi-join reduction (reduce.hpp:47-74)
+  if (!opt.assume_reduced) {
+    for (int i : preorder) check_nonempty(*nodes[i]);
+    for (auto it = preorder.rbegin(); it != preorder.rend(); ++it)
+      for (int c : nodes[*it]->children) {
+        semi_join(ctx, *nodes[*it], *nodes[c], nodes[c]->pattr, code);
+        check_nonempty(*nodes[*it]);
+      }
+    for (int i : preorder)
+      for (int c : nodes[i]->children) {
+        semi_join(ctx, *nodes[c], *nodes[i], nodes[c]->pattr, code);
+        check_nonempty(*nodes[c]);
+      }
+  }
+
+  // ---- K1: own-key grouping per relation
+  for (auto& np : nodes) {
+    NodeState& n = *np;
+    n.own = make_spec(n.key_attr, code,
+                      [&](int a) {
+                        return (int)(std::find(n.key_attr.begin(),
+                                               n.key_attr.end(), a) -
+                                     n.key_attr.begin());
+                      },
+                      &n.own_bits, "relation " + n.name);
+    DevArray<uint64_t> pk(n.rows, st);
+    DevArray<int> iota;
+    if (n.rows) {
+      if (n.has_sel) {
+        k_pack_sel<<<grid1d(ctx, n.rows), 256, 0, st>>>(n.keys, n.n_key,
+                                                        n.sel.get(), n.rows,
+                                                        n.own, pk.get());
+        FG_LAUNCHED(ctx);
+        FG_KERNEL_CHECK();
+      } else {
+        iota.alloc(n.rows, st);
+        launch_pack_keys(ctx, n.keys, n.rows, n.n_key, n.own, pk.get(),
+                         iota.get());
+      }
+    }
+    group_sorted(ctx, pk.get(), n.rows, n.own_bits,
+                 n.has_sel ? n.sel.get() : iota.get(), n.grp);
+    n.sizes.alloc(n.grp.G, st);
+    launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
+  }
+  // Parent-key grouping of own segments (the std::map regroupings of
+  // counts.hpp:121-130 and figaro.hpp:236-239).
+  for (auto& np : nodes) {
+    NodeState& n = *np;
+    if (n.parent < 0) continue;
+    int pbits = 0;
+    n.par = make_spec(n.pattr, code,
+                      [&](int a) {
+                        const int f = (int)(std::find(n.key_attr.begin(),
+                                                      n.key_attr.end(), a) -
+                                            n.key_attr.begin());
+                        return n.own.shift[f];
+                      },
+                      &pbits, "relation " + n.name + " (parent key)");
+    const int64_t G = n.grp.G;
+    DevArray<uint64_t> ppk(G, st);
+    launch_project(ctx, n.grp.uniq.get(), G, n.par, ppk.get());
+    DevArray<int> iota(G, st);
+    launch_iota(ctx, iota.get(), G);
+    GroupOut pg;
+    group_sorted(ctx, ppk.get(), G, pbits, iota.get(), pg, true);
+    n.P = pg.G;
+    n.pa_perm = std::move(pg.perm);
+    n.pa_begins = std::move(pg.begins);
+    n.upk = std::move(pg.uniq);
+    n.pidx.alloc(G, st);
+    DevArray<int> flags(G, st), scan(G, st);
+    launch_run_ids(ctx, pg.sorted.get(), n.pa_perm.get(), G, flags.get(),
+                   scan.get(), n.pidx.get());
+    if (n.children.empty() && n.P != G)
+      fail(FG_E_INTEGRITY, "relation " + n.name +
+                               ": leaf keys do not match its parent attributes");
+  }
+  // Edge lookups: own segment of i -> parent-key index of child c.
+  for (auto& np : nodes) {
+    NodeState& n = *np;
+    for (int c : n.children) {
+      NodeState& ch = *nodes[c];
+      PackSpec proj = make_spec(ch.pattr, code,
+                                [&](int a) {
+                                  const int f = (int)(std::find(n.key_attr.begin(),
+                                                                n.key_attr.end(), a) -
+                                                      n.key_attr.begin());
+                                  return n.own.shift[f];
+                                },
+                                nullptr, "edge " + n.name + "-" + ch.name);
+      DevArray<int> l(n.grp.G, st);
+      launch_lookup(ctx, n.grp.uniq.get(), n.grp.G, proj, ch.upk.get(), ch.P,
+                    l.get(), ctx.status.get());
+      n.lidx.push_back(std::move(l));
+    }
+  }
+  FG_CUDA(cudaEventRecord(ev.e[2], st));
+
+  // ---- K2: counts (counts.hpp:92-224)
+  for (auto& np : nodes) {
+    NodeState& n = *np;
+    n.theta.alloc(n.grp.G, st);
+    n.fjs.alloc(n.grp.G, st);
+    n.circ.alloc(n.grp.G, st);
+    n.phi_down.alloc(n.P, st);
+    n.phi_up.alloc(n.P, st);
+    n.phi_down.zero();
+    n.phi_up.zero();
+  }
+  auto links = [&](NodeState& n) {
+    ChildLinks ch{};
+    ch.n = (int)n.children.size();
+    if (ch.n > kMaxChildren) fail(FG_E_UNSUPPORTED, "more than 16 children");
+    for (int k = 0; k < ch.n; ++k) {
+      NodeState& c = *nodes[n.children[k]];
+      ch.lidx[k] = n.lidx[k].get();
+      ch.phi_down[k] = c.phi_down.get();
+      ch.phi_up[k] = c.phi_up.get();
+    }
+    return ch;
+  };
+  for (auto it = preorder.rbegin(); it != preorder.rend(); ++it) {
+    NodeState& n = *nodes[*it];
+    launch_theta(ctx, n.sizes.get(), n.grp.G, links(n),
+                 n.parent >= 0 ? n.pidx.get() : nullptr, n.phi_down.get(),
+                 n.theta.get(), ctx.status.get());
+  }
+  for (int i : preorder) {
+    NodeState& n = *nodes[i];
+    launch_fjs(ctx, n.sizes.get(), n.theta.get(), n.grp.G,
+               n.parent >= 0 ? n.pidx.get() : nullptr, n.phi_up.get(), links(n),
+               n.fjs.get(), n.circ.get(), ctx.status.get());
+    for (int c : n.children)
+      launch_up_div(ctx, nodes[c]->phi_up.get(), nodes[c]->phi_down.get(),
+                    nodes[c]->P, ctx.status.get());
+  }
+  FG_CUDA(cudaEventRecord(ev.e[3], st));
+  check_status(ctx, "compute_counts");
+
+  // ---- K3/K4/K5: the FiGaRo transform (figaro.hpp:166-329)
+  for (auto it = preorder.rbegin(); it != preorder.rend(); ++it) {
+    const int i = *it;
+    NodeState& n = *nodes[i];
+    const bool is_root = n.parent < 0;
+    const bool is_leaf = n.children.empty();
+    const int64_t G = n.grp.G;
+    n.width = lay.sub_end[i] - lay.sub_begin[i];
+    n.S.alloc(G * n.width, st);
+    if (!is_leaf) n.S.zero();
+    n.scale.alloc(G, st);
+    const int64_t n_tails = n.rows - G;
+    if (n.w > 0 && n_tails > 0) n.tails.alloc(n_tails * n.w, st);
+    HeadTailArgs a;
+    a.data = n.data;
+    a.ld = n.w;
+    a.w = n.w;
+    a.perm = n.grp.perm.get();
+    a.begins = n.grp.begins.get();
+    a.n_seg = G;
+    a.n_rows = n.rows;
+    a.tail_count = n.circ.get();
+    a.head_index = (is_leaf && !is_root) ? n.pidx.get() : nullptr;
+    a.heads = n.w > 0 ? n.S.get() : nullptr;
+    a.ldh = n.width;
+    a.tails = n.tails.get();
+    a.ldt = n.w;
+    a.scales = n.scale.get();
+    run_heads_tails(ctx, a);
+    if (!is_leaf) {
+      JoinArgs j{};
+      j.G = G;
+      j.own_w = n.w;
+      j.S = n.S.get();
+      j.width = n.width;
+      j.scale = n.scale.get();
+      j.n_children = (int)n.children.size();
+      for (int k = 0; k < j.n_children; ++k) {
+        NodeState& c = *nodes[n.children[k]];
+        j.lidx[k] = n.lidx[k].get();
+        j.child_S[k] = c.sum_S;
+        j.child_scale[k] = c.sum_scale;
+        j.child_w[k] = (int)c.width;
+        j.child_off[k] = (int)(lay.sub_begin[n.children[k]] - lay.sub_begin[i]);
+      }
+      launch_join(ctx, j);
+    }
+    if (!is_root && !is_leaf) {
+      n.Sq.alloc(n.P * n.width, st);
+      n.scale_q.alloc(n.P, st);
+      if (n.width > 0 && G > n.P) n.ptails.alloc((G - n.P) * n.width, st);
+      HeadTailArgs b;
+      b.data = n.S.get();
+      b.ld = n.width;
+      b.w = (int)n.width;
+      b.perm = n.pa_perm.get();
+      b.begins = n.pa_begins.get();
+      b.n_seg = n.P;
+      b.n_rows = G;
+      b.weights = n.scale.get();
+      b.tail_count = n.phi_up.get();
+      b.scale_count = n.phi_down.get();
+      b.heads = n.width > 0 ? n.Sq.get() : nullptr;
+      b.ldh = n.width;
+      b.tails = n.ptails.get();
+      b.ldt = n.width;
+      b.scales = n.scale_q.get();
+      run_heads_tails(ctx, b);
+      n.sum_S = n.Sq.get();
+      n.sum_scale = n.scale_q.get();
+    } else {
+      n.sum_S = n.S.get();
+      n.sum_scale = n.scale.get();
+    }
+  }
+  FG_CUDA(cudaEventRecord(ev.e[4], st));
+
+  // ---- R0 spans in figaro()'s block order, then K6/K7
+  std::vector<SpanInfo>& spans = saved->spans;
+  std::function<void(int)> collect = [&](int i) {
+    NodeState& n = *nodes[i];
+    if (n.tails.size())
+      spans.push_back({i, lay.node_offset[i], n.rows - n.grp.G, n.w,
+                       n.tails.get()});
+    for (int c : n.children) collect(c);
+    if (n.ptails.size())
+      spans.push_back({i, lay.sub_begin[i], n.grp.G - n.P, n.width,
+                       n.ptails.get()});
+    if (n.parent < 0 && n.width > 0 && n.grp.G > 0)
+      spans.push_back({i, lay.sub_begin[i], n.grp.G, n.width, n.S.get()});
+  };
+  collect(root);
+  int64_t r0_rows = 0;
+  std::vector<Span> tsq;
+  for (const auto& s : spans) {
+    r0_rows += s.rows;
+    tsq.push_back({s.data, s.rows, s.cols, (int)s.cols, (int)s.col_begin});
+  }
+  const int N = (int)lay.total;
+  DevArray<double> Rdev;
+  double* Rd = R_out;
+  if (opt.memory == FG_MEM_HOST) {
+    Rdev.alloc((size_t)N * N, st);
+    Rd = Rdev.get();
+  }
+  tsqr(ctx, tsq, N, Rd);
+  FG_CUDA(cudaEventRecord(ev.e[5], st));
+  if (opt.memory == FG_MEM_HOST && N > 0)
+    FG_CUDA(cudaMemcpyAsync(R_out, Rd, sizeof(double) * N * N,
+                            cudaMemcpyDeviceToHost, st));
+  FG_CUDA(cudaStreamSynchronize(st));
+  FG_CUDA(cudaGetLastError());
+
+  if (res) {
+    res->data_columns = N;
+    int64_t m = 0;
+    for (auto& n : nodes) m += n->rows;
+    res->input_rows = m;
+    res->r0_rows = r0_rows;
+    res->seconds_group = ev.ms(1, 2);
+    res->seconds_counts = ev.ms(2, 3);
+    res->seconds_figaro = ev.ms(3, 4);
+    res->seconds_postprocess = ev.ms(4, 5);
+    res->seconds_total = ev.ms(0, 5);
+    res->kernels = ctx.launches - launches0;
+  }
+  // Keep the inspection state; drop the bulky buffers unless R0 is wanted.
+  saved->have_r0 = opt.keep_r0 != 0;
+  for (auto& n : nodes) {
+    n->keys_own.release();
+    n->data_own.release();
+    n->sel.release();
+    if (!opt.keep_r0) {
+      n->S.release();
+      n->Sq.release();
+      n->tails.release();
+      n->ptails.release();
+    }
+  }
+  if (!opt.keep_r0) spans.clear();
+  delete ctx.saved;
+  ctx.saved = saved.release();
+}
+
+fg_status guard(fg_ctx* c, const std::function<void()>& f) {
+  Context* ctx = reinterpret_cast<Context*>(c);
+  if (!ctx) return FG_E_ARG;
+  try {
+    FG_CUDA(cudaSetDevice(ctx->device));
+    f();
+    ctx->last_error = "ok";
+    return FG_OK;
+  } catch (const Failure& e) {
+    ctx->last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->last_error = e.what();
+    return FG_E_ARG;
+  }
+}
+
+NodeState& node_at(Context& ctx, int32_t node) {
+  if (!ctx.saved) fail(FG_E_ARG, "no pipeline result");
+  if (node < 0 || node >= (int)ctx.saved->nodes.size())
+    fail(FG_E_ARG, "node index out of range");
+  return *ctx.saved->nodes[node];
+}
+
+}  // namespace
+}  // namespace fg
+
+using fg::Context;
+using fg::fail;
+
+extern "C" {
+
+int32_t fg_version(void) { return FIGARO_CUDA_VERSION; }
+
+void fg_options_default(fg_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->assume_reduced = 0;
+  o->engine = FG_ENGINE_THIN;
+  o->memory = FG_MEM_DEVICE;
+  o->keep_r0 = 0;
+  o->fuse = 0;
+}
+
+fg_status fg_ctx_create(int32_t device, fg_ctx** out) {
+  if (!out) return FG_E_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return FG_E_CUDA;
+  if (device < 0 || device >= n) return FG_E_ARG;
+  auto* ctx = new Context();
+  ctx->device = device;
+  try {
+    FG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    FG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+      delete ctx;
+      return FG_E_CUDA;  // built for sm_100a only
+    }
+    ctx->sm_count = prop.multiProcessorCount;
+    ctx->smem_optin = prop.sharedMemPerBlockOptin;
+    FG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    // Keep freed pool memory: no OS round trips in steady state.
+    cudaMemPool_t pool;
+    FG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    FG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    ctx->status.alloc(1, ctx->stream);
+    ctx->status.zero();
+    FG_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (const fg::Failure&) {
+    delete ctx;
+    return FG_E_CUDA;
+  }
+  *out = reinterpret_cast<fg_ctx*>(ctx);
+  return FG_OK;
+}
+
+fg_status fg_ctx_destroy(fg_ctx* c) {
+  Context* ctx = reinterpret_cast<Context*>(c);
+  if (!ctx) return FG_OK;
+  cudaSetDevice(ctx->device);
+  delete ctx->saved;
+  ctx->saved = nullptr;
+  ctx->status.release();
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return FG_OK;
+}
+
+fg_status fg_ctx_set_stream(fg_ctx* c, void* s) {
+  return fg::guard(c, [&] {
+    Context* ctx = reinterpret_cast<Context*>(c);
+    FG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (s) {
+      ctx->stream = static_cast<cudaStream_t>(s);
+      ctx->own_stream = false;
+    } else {
+      FG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+  });
+}
+
+void* fg_ctx_stream(fg_ctx* c) {
+  Context* ctx = reinterpret_cast<Context*>(c);
+  return ctx ? ctx->stream : nullptr;
+}
+
+const char* fg_last_error(fg_ctx* c) {
+  Context* ctx = reinterpret_cast<Context*>(c);
+  return ctx ? ctx->last_error.c_str() : "null context";
+}
+
+int64_t fg_kernel_launches(fg_ctx* c) {
+  Context* ctx = reinterpret_cast<Context*>(c);
+  return ctx ? ctx->launches : 0;
+}
+
+fg_status fg_run_pipeline(fg_ctx* c, int32_t n_rel, const fg_relation* rels,
+                          int32_t root, const int32_t* parent,
+                          const fg_options* options, double* R_out,
+                          fg_result* result) {
+  return fg::guard(c, [&] {
+    fg_options o;
+    fg_options_default(&o);
+    if (options) o = *options;
+    if (!R_out) fail(FG_E_ARG, "R_out is null");
+    fg::run(*reinterpret_cast<Context*>(c), n_rel, rels, root, parent, o,
+            R_out, result);
+  });
+}
+
+fg_status fg_get_sizes(fg_ctx* c, int32_t node, int64_t* G, int64_t* P) {
+  return fg::guard(c, [&] {
+    auto& n = fg::node_at(*reinterpret_cast<Context*>(c), node);
+    if (G) *G = n.grp.G;
+    if (P) *P = n.parent >= 0 ? n.P : 0;
+  });
+}
+
+fg_status fg_get_segments(fg_ctx* c, int32_t node, int64_t* begins) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    auto& n = fg::node_at(ctx, node);
+    std::vector<int> h(n.grp.G + 1, 0);
+    if (n.grp.begins.size())
+      FG_CUDA(cudaMemcpy(h.data(), n.grp.begins.get(), h.size() * sizeof(int),
+                         cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < h.size(); ++i) begins[i] = h[i];
+  });
+}
+
+fg_status fg_get_keys(fg_ctx* c, int32_t node, int32_t parent_keys,
+                      int64_t* out) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    auto& n = fg::node_at(ctx, node);
+    const bool par = parent_keys != 0;
+    if (par && n.parent < 0) return;
+    const int64_t cnt = par ? n.P : n.grp.G;
+    fg::PackSpec spec = par ? n.par : n.own;
+    if (spec.n == 0 || cnt == 0) return;
+    fg::DevArray<int64_t> d(cnt * spec.n, ctx.stream);
+    fg::launch_unpack(ctx, par ? n.upk.get() : n.grp.uniq.get(), cnt, spec,
+                      d.get());
+    FG_CUDA(cudaMemcpyAsync(out, d.get(), d.bytes(), cudaMemcpyDeviceToHost,
+                            ctx.stream));
+    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+fg_status fg_get_counts(fg_ctx* c, int32_t node, int32_t kind, uint64_t* out) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    auto& n = fg::node_at(ctx, node);
+    const fg::DevArray<uint64_t>* src = nullptr;
+    switch (kind) {
+      case FG_ROWS_PER_KEY: src = &n.sizes; break;
+      case FG_THETA_DOWN: src = &n.theta; break;
+      case FG_FULL_JOIN_SIZE: src = &n.fjs; break;
+      case FG_PHI_CIRC: src = &n.circ; break;
+      case FG_PHI_DOWN: src = &n.phi_down; break;
+      case FG_PHI_UP: src = &n.phi_up; break;
+      default: fail(FG_E_ARG, "unknown count kind");
+    }
+    if (kind >= FG_PHI_DOWN && n.parent < 0) return;
+    if (src->size())
+      FG_CUDA(cudaMemcpy(out, src->get(), src->bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+fg_status fg_get_permutation(fg_ctx* c, int32_t node, int32_t* out) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    auto& n = fg::node_at(ctx, node);
+    if (n.grp.perm.size())
+      FG_CUDA(cudaMemcpy(out, n.grp.perm.get(), n.grp.perm.bytes(),
+                         cudaMemcpyDeviceToHost));
+  });
+}
+
+fg_status fg_get_r0_span_count(fg_ctx* c, int32_t* n_spans) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    if (!ctx.saved || !ctx.saved->have_r0) fail(FG_E_ARG, "R0 was not kept");
+    *n_spans = (int32_t)ctx.saved->spans.size();
+  });
+}
+
+fg_status fg_get_r0_span(fg_ctx* c, int32_t idx, int32_t* node,
+                         int64_t* col_begin, int64_t* rows, int64_t* cols,
+                         double* out) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    if (!ctx.saved || !ctx.saved->have_r0) fail(FG_E_ARG, "R0 was not kept");
+    if (idx < 0 || idx >= (int)ctx.saved->spans.size())
+      fail(FG_E_ARG, "span index out of range");
+    const auto& s = ctx.saved->spans[idx];
+    if (node) *node = s.node;
+    if (col_begin) *col_begin = s.col_begin;
+    if (rows) *rows = s.rows;
+    if (cols) *cols = s.cols;
+    if (out && s.rows * s.cols) {
+      if (!s.data) fail(FG_E_ARG, "final span is not kept");
+      FG_CUDA(cudaMemcpy(out, s.data, sizeof(double) * s.rows * s.cols,
+                         cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+fg_status fg_group_keys(fg_ctx* c, const uint64_t* keys, int64_t n,
+                        int32_t bits, int32_t* perm, int32_t* begins,
+                        uint64_t* uniq, int64_t* G) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    if (bits < 0 || bits > 64) fail(FG_E_ARG, "bits out of range");
+    if (n > INT_MAX) fail(FG_E_UNSUPPORTED, "more than 2^31-1 keys");
+    fg::DevArray<int> iota(n, ctx.stream);
+    fg::launch_iota(ctx, iota.get(), n);
+    fg::GroupOut g;
+    fg::group_sorted(ctx, keys, n, bits, iota.get(), g);
+    if (n) {
+      FG_CUDA(cudaMemcpyAsync(perm, g.perm.get(), n * sizeof(int),
+                              cudaMemcpyDeviceToDevice, ctx.stream));
+    }
+    FG_CUDA(cudaMemcpyAsync(begins, g.begins.get(), (g.G + 1) * sizeof(int),
+                            cudaMemcpyDeviceToDevice, ctx.stream));
+    if (g.G)
+      FG_CUDA(cudaMemcpyAsync(uniq, g.uniq.get(), g.G * sizeof(uint64_t),
+                              cudaMemcpyDeviceToDevice, ctx.stream));
+    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+    *G = g.G;
+  });
+}
+
+fg_status fg_heads_tails(fg_ctx* c, const double* data, int64_t ld, int32_t w,
+                         const int32_t* perm, const int32_t* begins,
+                         int64_t n_seg, const double* weights,
+                         const uint64_t* tail_count, double* heads,
+                         int64_t ldh, double* tails, int64_t ldt,
+                         double* scales) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    if (n_seg < 0 || w < 0) fail(FG_E_ARG, "negative size");
+    int n_rows = 0;
+    if (n_seg > 0)
+      FG_CUDA(cudaMemcpy(&n_rows, begins + n_seg, sizeof(int),
+                         cudaMemcpyDeviceToHost));
+    fg::HeadTailArgs a;
+    a.data = data;
+    a.ld = ld;
+    a.w = w;
+    a.perm = perm;
+    a.begins = begins;
+    a.n_seg = n_seg;
+    a.n_rows = n_rows;
+    a.weights = weights;
+    a.tail_count = tail_count;
+    a.heads = heads;
+    a.ldh = ldh;
+    a.tails = tails;
+    a.ldt = ldt;
+    a.scales = scales;
+    fg::run_heads_tails(ctx, a);
+    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+fg_status fg_tsqr(fg_ctx* c, int32_t n_blocks, const fg_block* blocks,
+                  int32_t n, double* R_out) {
+  return fg::guard(c, [&] {
+    Context& ctx = *reinterpret_cast<Context*>(c);
+    std::vector<fg::Span> spans;
+    for (int i = 0; i < n_blocks; ++i) {
+      const fg_block& b = blocks[i];
+      if (b.col_begin < 0 || b.cols < 0 || b.col_begin + b.cols > n)
+        fail(FG_E_ARG, "block exceeds column count");
+      spans.push_back({b.data, b.rows, b.ld, b.cols, b.col_begin});
+    }
+    fg::tsqr(ctx, spans, n, R_out);
+    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+}  // extern "C"
