@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <string>
 #include <utility>
 #include <vector>
@@ -47,8 +48,66 @@ enum : unsigned {
 
 struct Context;
 
-// Stream-ordered device buffer (cudaMallocAsync from the device pool, which
-// is configured to keep memory, so steady-state calls do not hit the OS).
+// Caching device allocator owned by a context.  All device work of a context
+// is ordered on its one stream, so a block freed by an earlier stage can be
+// handed to a later stage without synchronisation.  Steady-state calls with
+// the same shapes never reach cudaMalloc.
+class BlockCache {
+ public:
+  void* get(size_t bytes) {
+    bytes = round(bytes);
+    auto it = free_.lower_bound(bytes);
+    if (it != free_.end() && it->first <= bytes + bytes / 4 + (1 << 20)) {
+      void* p = it->second;
+      size_t b = it->first;
+      free_.erase(it);
+      live_[p] = b;
+      return p;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      trim();
+      FG_CUDA(cudaMalloc(&p, bytes));
+    }
+    live_[p] = bytes;
+    reserved_ += bytes;
+    return p;
+  }
+  void put(void* p) {
+    auto it = live_.find(p);
+    if (it == live_.end()) return;
+    free_.emplace(it->second, p);
+    live_.erase(it);
+  }
+  // Returns cached blocks to the driver (synchronises the device).
+  void trim() {
+    if (free_.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& kv : free_) {
+      cudaFree(kv.second);
+      reserved_ -= kv.first;
+    }
+    free_.clear();
+  }
+  size_t reserved() const { return reserved_; }
+
+ private:
+  static size_t round(size_t b) {
+    if (b < (1 << 20)) return (b + 511) & ~size_t(511);
+    return (b + (2 << 20) - 1) & ~size_t((2 << 20) - 1);
+  }
+  std::multimap<size_t, void*> free_;
+  std::map<void*, size_t> live_;
+  size_t reserved_ = 0;
+};
+
+// The cache of the context currently running on this thread (set by the C
+// entry points); DevArray allocates from it.
+BlockCache*& current_cache();
+
+// Device buffer drawn from the current context's BlockCache.
 template <class T>
 class DevArray {
  public:
@@ -70,10 +129,14 @@ class DevArray {
     release();
     stream_ = s;
     n_ = n;
-    if (n) FG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    if (n) {
+      cache_ = current_cache();
+      if (!cache_) fail(FG_E_ARG, "device allocation outside a context");
+      p_ = static_cast<T*>(cache_->get(n * sizeof(T)));
+    }
   }
   void release() {
-    if (p_) cudaFreeAsync(p_, stream_);
+    if (p_ && cache_) cache_->put(p_);
     p_ = nullptr;
     n_ = 0;
   }
@@ -89,10 +152,12 @@ class DevArray {
     std::swap(p_, o.p_);
     std::swap(n_, o.n_);
     std::swap(stream_, o.stream_);
+    std::swap(cache_, o.cache_);
   }
   T* p_ = nullptr;
   size_t n_ = 0;
   cudaStream_t stream_ = nullptr;
+  BlockCache* cache_ = nullptr;
 };
 
 struct LaunchCounter {
@@ -110,6 +175,7 @@ struct Context {
   size_t smem_optin = 0;
   std::string last_error = "ok";
   int64_t launches = 0;
+  BlockCache cache;           // declared before every DevArray member
   DevArray<unsigned> status;  // device status word
   // Results of the last pipeline run, kept for fg_get_* inspection.
   struct Saved;

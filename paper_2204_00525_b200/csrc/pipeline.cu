@@ -11,7 +11,9 @@
 //   postprocess_thin + normalize_signs     -> K6/K7 (tsqr.cu)
 // Device phases are timed with CUDA events on the context stream.
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -395,6 +397,19 @@ void check_status(Context& ctx, const char* phase) {
   fail(FG_E_INTEGRITY, p + ": inconsistent counts");
 }
 
+// Host-side stage timer, enabled with FG_TRACE=1 (prints to stderr).
+struct Trace {
+  bool on = getenv("FG_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fg] %-28s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 struct Events {
   cudaEvent_t e[6];
   Events() { for (auto& x : e) cudaEventCreate(&x); }
@@ -443,6 +458,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   if (lay.total > 128)
     fail(FG_E_UNSUPPORTED, "more than 128 data columns in total");
 
+  Trace tr;
   Events ev;
   FG_CUDA(cudaEventRecord(ev.e[0], st));
 
@@ -468,6 +484,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   }
   FG_CUDA(cudaEventRecord(ev.e[1], st));
   ctx.status.zero();
+  tr.mark("setup+upload");
 
   // ---- attribute encodings (global, per attribute name)
   std::map<std::string, int> attr_id;
@@ -510,6 +527,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     }
   }
 
+  tr.mark("encode (minmax sync)");
   // ---- semi-join reduction (reduce.hpp:47-74)
   if (!opt.assume_reduced) {
     for (int i : preorder) check_nonempty(*nodes[i]);
@@ -555,6 +573,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     n.sizes.alloc(n.grp.G, st);
     launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
   }
+  tr.mark("own grouping");
   // Parent-key grouping of own segments (the std::map regroupings of
   // counts.hpp:121-130 and figaro.hpp:236-239).
   for (auto& np : nodes) {
@@ -588,6 +607,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       fail(FG_E_INTEGRITY, "relation " + n.name +
                                ": leaf keys do not match its parent attributes");
   }
+  tr.mark("parent grouping");
   // Edge lookups: own segment of i -> parent-key index of child c.
   for (auto& np : nodes) {
     NodeState& n = *np;
@@ -648,7 +668,9 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
                     nodes[c]->P, ctx.status.get());
   }
   FG_CUDA(cudaEventRecord(ev.e[3], st));
+  tr.mark("lookups+counts enqueue");
   check_status(ctx, "compute_counts");
+  tr.mark("counts status sync");
 
   // ---- K3/K4/K5: the FiGaRo transform (figaro.hpp:166-329)
   for (auto it = preorder.rbegin(); it != preorder.rend(); ++it) {
@@ -726,6 +748,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     }
   }
   FG_CUDA(cudaEventRecord(ev.e[4], st));
+  tr.mark("figaro enqueue");
 
   // ---- R0 spans in figaro()'s block order, then K6/K7
   std::vector<SpanInfo>& spans = saved->spans;
@@ -756,12 +779,14 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     Rd = Rdev.get();
   }
   tsqr(ctx, tsq, N, Rd);
+  tr.mark("tsqr enqueue");
   FG_CUDA(cudaEventRecord(ev.e[5], st));
   if (opt.memory == FG_MEM_HOST && N > 0)
     FG_CUDA(cudaMemcpyAsync(R_out, Rd, sizeof(double) * N * N,
                             cudaMemcpyDeviceToHost, st));
   FG_CUDA(cudaStreamSynchronize(st));
   FG_CUDA(cudaGetLastError());
+  tr.mark("final sync");
 
   if (res) {
     res->data_columns = N;
@@ -794,9 +819,17 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   ctx.saved = saved.release();
 }
 
+// RAII: makes ctx's BlockCache the allocation source of this thread.
+struct CacheScope {
+  BlockCache* prev;
+  explicit CacheScope(Context* c) : prev(current_cache()) { current_cache() = &c->cache; }
+  ~CacheScope() { current_cache() = prev; }
+};
+
 fg_status guard(fg_ctx* c, const std::function<void()>& f) {
   Context* ctx = reinterpret_cast<Context*>(c);
   if (!ctx) return FG_E_ARG;
+  CacheScope scope(ctx);
   try {
     FG_CUDA(cudaSetDevice(ctx->device));
     f();
@@ -819,6 +852,12 @@ NodeState& node_at(Context& ctx, int32_t node) {
 }
 
 }  // namespace
+
+BlockCache*& current_cache() {
+  static thread_local BlockCache* c = nullptr;
+  return c;
+}
+
 }  // namespace fg
 
 using fg::Context;
@@ -846,6 +885,7 @@ fg_status fg_ctx_create(int32_t device, fg_ctx** out) {
   if (device < 0 || device >= n) return FG_E_ARG;
   auto* ctx = new Context();
   ctx->device = device;
+  fg::current_cache() = &ctx->cache;
   try {
     FG_CUDA(cudaSetDevice(device));
     cudaDeviceProp prop{};
@@ -866,9 +906,11 @@ fg_status fg_ctx_create(int32_t device, fg_ctx** out) {
     ctx->status.zero();
     FG_CUDA(cudaStreamSynchronize(ctx->stream));
   } catch (const fg::Failure&) {
+    fg::current_cache() = nullptr;
     delete ctx;
     return FG_E_CUDA;
   }
+  fg::current_cache() = nullptr;
   *out = reinterpret_cast<fg_ctx*>(ctx);
   return FG_OK;
 }
@@ -877,10 +919,13 @@ fg_status fg_ctx_destroy(fg_ctx* c) {
   Context* ctx = reinterpret_cast<Context*>(c);
   if (!ctx) return FG_OK;
   cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  fg::current_cache() = &ctx->cache;
   delete ctx->saved;
   ctx->saved = nullptr;
   ctx->status.release();
-  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->cache.trim();
+  fg::current_cache() = nullptr;
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return FG_OK;

@@ -4,18 +4,24 @@
 // absorb + tournament merge (postprocess.hpp:70-169) and normalize_signs
 // (postprocess.hpp:173-190).  The reference rotates row by row with Givens;
 // here each CTA owns an upper-triangular accumulator R (shared memory) and
-// absorbs B-row tiles of one span with a structured Householder QR of
-// [R; X] (the LAPACK tpqrt shape: reflector k touches row k of R and all B
-// rows of the tile), so a tile costs 2 B W^2 flops.  The tile lives in
-// registers in a column-owner layout: TC column groups x TR row lanes, each
-// thread holding RPT rows x CPT columns.  Columns are dealt to groups in
-// mirrored pairs (c, 2TC-1-c, ...), so every group keeps the same amount of
-// trailing work as the active width shrinks.  One barrier per column.
+// absorbs B-row tiles with a structured Householder QR of [R; X] (the LAPACK
+// tpqrt shape: reflector k touches row k of R and the B tile rows), 2 B W^2
+// flops per tile.
 //
-// Spans are factored in parallel by persistent CTAs (level 0); the partial
-// factors are embedded at their column offsets and merged by further
-// launches of the same kernel until one CTA remains; its R is
-// sign-normalised (positive diagonal, strictly-lower entries exactly zero).
+// Tile pipeline: rows are staged global -> shared with cp.async (LDGSTS,
+// coalesced, zero-filled outside the span's column range) one tile ahead of
+// the compute, then moved into registers in a column-owner layout: TC column
+// groups x TR row lanes, each thread holding RPT rows x CPT columns.  Columns
+// are dealt to groups in mirrored pairs (c, 2TC-1-c, ...) so the trailing
+// work stays balanced as the active width shrinks.  One CTA barrier per
+// column; reductions over the TR lanes of a group are xor-shuffles.
+//
+// Level 0 factors each span with persistent CTAs; the partial factors are
+// then treated as rows of one n-wide matrix (embedded at their column
+// offsets) and merged by the same kernel until one CTA remains.  The last R
+// is sign-normalised (positive diagonal, strictly-lower entries exactly 0).
+#include <cuda_pipeline.h>
+
 #include <algorithm>
 
 #include "launchers.cuh"
@@ -24,21 +30,13 @@ namespace fg {
 
 namespace {
 
-struct TsqrSeg {
+struct SegDev {
   const double* data;
   int64_t rows;
   int64_t ld;
   int cols;
   int col_begin;
-  int64_t tile0;  // first global tile of this segment
-};
-
-constexpr int kMaxSegs = 64;
-
-struct TsqrParams {
-  int nseg;
-  int64_t total_tiles;
-  TsqrSeg seg[kMaxSegs];
+  int64_t row0;  // first row of this segment in the concatenated row space
 };
 
 template <int W_, int TC_, int TR_, int RPT_>
@@ -51,8 +49,11 @@ struct Cfg {
   static constexpr int GPW = 32 / TR;
   static constexpr int NT = TC * TR;
   static constexpr int B = TR * RPT;
+  static constexpr int LDS = W + 1;  // padded staging row (bank spread)
   static_assert(W % TC == 0, "W % TC");
   static_assert(TC % GPW == 0, "TC % GPW");
+  static constexpr size_t smem_doubles = W * W + 2 * B + 2 + B * LDS;
+  static constexpr size_t smem_bytes = smem_doubles * 8 + B * sizeof(int);
 };
 
 template <class C>
@@ -67,13 +68,57 @@ __device__ __forceinline__ double group_sum(double x, unsigned mask) {
   return x;
 }
 
+// Issues the cp.async copies of tile `t` (rows t*B .. t*B+B-1 of the
+// concatenated segment rows) into `stage`.
+template <class C>
+__device__ __forceinline__ void stage_tile(const SegDev* __restrict__ segs,
+                                           int nseg, int64_t total_rows,
+                                           int64_t t, double* stage,
+                                           int* rowseg) {
+  const int64_t r0 = t * C::B;
+  for (int row = threadIdx.x; row < C::B; row += C::NT) {
+    const int64_t gr = r0 + row;
+    int s = -1;
+    if (gr < total_rows) {
+      int lo = 0, hi = nseg;  // last segment with row0 <= gr
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (segs[mid].row0 <= gr) lo = mid; else hi = mid;
+      }
+      s = lo;
+    }
+    rowseg[row] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < C::B * C::W; e += C::NT) {
+    const int row = e / C::W;
+    const int col = e - row * C::W;
+    double* dst = stage + row * C::LDS + col;
+    const int s = rowseg[row];
+    if (s >= 0) {
+      const SegDev& sg = segs[s];
+      const int lc = col - sg.col_begin;
+      if (lc >= 0 && lc < sg.cols) {
+        __pipeline_memcpy_async(dst, sg.data + (r0 + row - sg.row0) * sg.ld + lc,
+                                sizeof(double));
+        continue;
+      }
+    }
+    *dst = 0.0;
+  }
+  __pipeline_commit();
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NT)
-    k_tsqr(const __grid_constant__ TsqrParams P, double* __restrict__ out) {
+    k_tsqr(const SegDev* __restrict__ segs, int nseg, int64_t total_rows,
+           int64_t total_tiles, double* __restrict__ out) {
   extern __shared__ __align__(16) double sm[];
-  double* R = sm;                       // W x W
-  double* vbuf = sm + C::W * C::W;      // 2 x B
-  double* taus = vbuf + 2 * C::B;       // 2
+  double* R = sm;                         // W x W
+  double* vbuf = R + C::W * C::W;         // 2 x B
+  double* taus = vbuf + 2 * C::B;         // 2
+  double* stage = taus + 2;               // B x LDS
+  int* rowseg = reinterpret_cast<int*>(stage + C::B * C::LDS);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -84,26 +129,22 @@ __global__ void __launch_bounds__(C::NT)
       C::TR == 32 ? 0xffffffffu : (((1u << C::TR) - 1u) << (gw * C::TR));
 
   for (int e = threadIdx.x; e < C::W * C::W; e += C::NT) R[e] = 0.0;
-  __syncthreads();
 
   double X[C::RPT][C::CPT];
+  int64_t t = blockIdx.x;
+  if (t < total_tiles) stage_tile<C>(segs, nseg, total_rows, t, stage, rowseg);
 
-  for (int64_t t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
-    int s = 0;
-    while (s + 1 < P.nseg && P.seg[s + 1].tile0 <= t) ++s;
-    const TsqrSeg& sg = P.seg[s];
-    const int64_t row0 = (t - sg.tile0) * C::B;
+  for (; t < total_tiles; t += gridDim.x) {
+    __pipeline_wait_prior(0);
+    __syncthreads();
 #pragma unroll
-    for (int i = 0; i < C::RPT; ++i) {
-      const int64_t row = row0 + i * C::TR + r;
+    for (int i = 0; i < C::RPT; ++i)
 #pragma unroll
-      for (int q = 0; q < C::CPT; ++q) {
-        const int lc = col_of<C>(q, c) - sg.col_begin;
-        X[i][q] = (row < sg.rows && lc >= 0 && lc < sg.cols)
-                      ? __ldg(sg.data + row * sg.ld + lc)
-                      : 0.0;
-      }
-    }
+      for (int q = 0; q < C::CPT; ++q)
+        X[i][q] = stage[(i * C::TR + r) * C::LDS + col_of<C>(q, c)];
+    __syncthreads();
+    if (t + gridDim.x < total_tiles)
+      stage_tile<C>(segs, nseg, total_rows, t + gridDim.x, stage, rowseg);
 
 #pragma unroll
     for (int qb = 0; qb < C::CPT; ++qb) {
@@ -112,10 +153,13 @@ __global__ void __launch_bounds__(C::NT)
         const int ck = (qb & 1) ? C::TC - 1 - within : within;
         double* vb = vbuf + (k & 1) * C::B;
         if (c == ck) {
-          double sig = 0.0;
+          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int i = 0; i < C::RPT; ++i) sig = fma(X[i][qb], X[i][qb], sig);
-          sig = group_sum<C>(sig, gmask);
+          for (int i = 0; i < C::RPT; i += 2) {
+            s0 = fma(X[i][qb], X[i][qb], s0);
+            if (i + 1 < C::RPT) s1 = fma(X[i + 1][qb], X[i + 1][qb], s1);
+          }
+          const double sig = group_sum<C>(s0 + s1, gmask);
           const double alpha = R[k * C::W + k];
           double tau = 0.0;
           if (sig > 0.0) {
@@ -141,10 +185,13 @@ __global__ void __launch_bounds__(C::NT)
           const int j = col_of<C>(q, c);
           if (j <= k) continue;
           const double rkj = R[k * C::W + j];
-          double d = 0.0;
+          double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-          for (int i = 0; i < C::RPT; ++i) d = fma(v[i], X[i][q], d);
-          d = group_sum<C>(d, gmask);
+          for (int i = 0; i < C::RPT; i += 2) {
+            d0 = fma(v[i], X[i][q], d0);
+            if (i + 1 < C::RPT) d1 = fma(v[i + 1], X[i + 1][q], d1);
+          }
+          const double d = group_sum<C>(d0 + d1, gmask);
           const double f = tau * (d + rkj);
 #pragma unroll
           for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
@@ -153,8 +200,8 @@ __global__ void __launch_bounds__(C::NT)
         }
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
   double* o = out + (int64_t)blockIdx.x * C::W * C::W;
   for (int e = threadIdx.x; e < C::W * C::W; e += C::NT) o[e] = R[e];
 }
@@ -170,11 +217,11 @@ __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
   }
 }
 
-using C4 = Cfg<4, 4, 32, 4>;
-using C8 = Cfg<8, 4, 32, 4>;
-using C16 = Cfg<16, 8, 16, 8>;
-using C32 = Cfg<32, 16, 16, 4>;
-using C64 = Cfg<64, 32, 8, 8>;
+using C4 = Cfg<4, 4, 32, 8>;
+using C8 = Cfg<8, 4, 32, 8>;
+using C16 = Cfg<16, 8, 16, 16>;
+using C32 = Cfg<32, 16, 16, 8>;
+using C64 = Cfg<64, 32, 8, 16>;
 using C128 = Cfg<128, 32, 8, 8>;
 
 int bucket(int w) {
@@ -184,68 +231,59 @@ int bucket(int w) {
 }
 
 template <class C>
-size_t smem_bytes() {
-  return sizeof(double) * (C::W * C::W + 2 * C::B + 2);
+int max_ctas(Context& ctx) {
+  FG_CUDA(cudaFuncSetAttribute(k_tsqr<C>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)C::smem_bytes));
+  int per_sm = 0;
+  FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsqr<C>,
+                                                        C::NT, C::smem_bytes));
+  return std::max(1, per_sm) * ctx.sm_count;
 }
 
-template <class C>
-int tile_rows() { return C::B; }
+struct Plan {
+  int B;
+  int cap;
+};
 
-int tile_rows_for(int W) {
+template <class C>
+Plan plan_of(Context& ctx) {
+  return {C::B, max_ctas<C>(ctx)};
+}
+
+Plan plan_for(Context& ctx, int W) {
   switch (W) {
-    case 4: return C4::B;
-    case 8: return C8::B;
-    case 16: return C16::B;
-    case 32: return C32::B;
-    case 64: return C64::B;
-    default: return C128::B;
+    case 4: return plan_of<C4>(ctx);
+    case 8: return plan_of<C8>(ctx);
+    case 16: return plan_of<C16>(ctx);
+    case 32: return plan_of<C32>(ctx);
+    case 64: return plan_of<C64>(ctx);
+    default: return plan_of<C128>(ctx);
   }
 }
 
 template <class C>
-int max_ctas(Context& ctx) {
-  const size_t smem = smem_bytes<C>();
-  FG_CUDA(cudaFuncSetAttribute(k_tsqr<C>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
-  int per_sm = 0;
-  FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsqr<C>,
-                                                        C::NT, smem));
-  return std::max(1, per_sm) * ctx.sm_count;
-}
-
-template <class C>
-void launch(Context& ctx, const TsqrParams& p, int grid, double* out) {
-  k_tsqr<C><<<grid, C::NT, smem_bytes<C>(), ctx.stream>>>(p, out);
+void launch(Context& ctx, const SegDev* segs, int nseg, int64_t rows,
+            int64_t tiles, int grid, double* out) {
+  k_tsqr<C><<<grid, C::NT, C::smem_bytes, ctx.stream>>>(segs, nseg, rows,
+                                                         tiles, out);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
 }
 
-int max_ctas_for(Context& ctx, int W) {
+void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
+                int64_t rows, int64_t tiles, int grid, double* out) {
   switch (W) {
-    case 4: return max_ctas<C4>(ctx);
-    case 8: return max_ctas<C8>(ctx);
-    case 16: return max_ctas<C16>(ctx);
-    case 32: return max_ctas<C32>(ctx);
-    case 64: return max_ctas<C64>(ctx);
-    default: return max_ctas<C128>(ctx);
+    case 4: launch<C4>(ctx, segs, nseg, rows, tiles, grid, out); break;
+    case 8: launch<C8>(ctx, segs, nseg, rows, tiles, grid, out); break;
+    case 16: launch<C16>(ctx, segs, nseg, rows, tiles, grid, out); break;
+    case 32: launch<C32>(ctx, segs, nseg, rows, tiles, grid, out); break;
+    case 64: launch<C64>(ctx, segs, nseg, rows, tiles, grid, out); break;
+    default: launch<C128>(ctx, segs, nseg, rows, tiles, grid, out); break;
   }
 }
 
-void launch_for(Context& ctx, int W, const TsqrParams& p, int grid,
-                double* out) {
-  switch (W) {
-    case 4: launch<C4>(ctx, p, grid, out); break;
-    case 8: launch<C8>(ctx, p, grid, out); break;
-    case 16: launch<C16>(ctx, p, grid, out); break;
-    case 32: launch<C32>(ctx, p, grid, out); break;
-    case 64: launch<C64>(ctx, p, grid, out); break;
-    default: launch<C128>(ctx, p, grid, out); break;
-  }
-}
-
-// A factor produced by one launch: `count` W x W matrices at `data`, whose
-// meaningful width is `cols`, placed at `col_begin`.
+// A batch of W x W partial factors, meaningful width `cols` at `col_begin`.
 struct Partial {
   const double* data;
   int count;
@@ -254,40 +292,28 @@ struct Partial {
   int col_begin;
 };
 
-// Factors a list of segments (all with the same bucket W); a CTA takes about
-// `tiles_per_cta` tiles.  Returns the number of W x W partial factors.
-int factor_segments(Context& ctx, int W, const std::vector<TsqrSeg>& segs,
-                    int64_t tiles_per_cta, DevArray<double>& out) {
-  const int B = tile_rows_for(W);
-  const int cap = max_ctas_for(ctx, W);
-  std::vector<TsqrParams> plans;
-  std::vector<int> grids;
-  int total = 0;
-  for (size_t i = 0; i < segs.size();) {
-    TsqrParams p{};
-    int64_t tiles = 0;
-    int n = 0;
-    for (; i < segs.size() && n < kMaxSegs; ++i) {
-      TsqrSeg s = segs[i];
-      s.tile0 = tiles;
-      tiles += ceil_div(s.rows, B);
-      p.seg[n++] = s;
-    }
-    p.nseg = n;
-    p.total_tiles = tiles;
-    const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>(cap, ceil_div(tiles, tiles_per_cta)));
-    plans.push_back(p);
-    grids.push_back(grid);
-    total += grid;
+// Factors the concatenation of `segs` (bucket W) with CTAs taking about
+// `tiles_per_cta` tiles each; returns the number of partial factors in out.
+int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_cta,
+           DevArray<double>& out) {
+  const Plan p = plan_for(ctx, W);
+  int64_t rows = 0;
+  for (auto& s : segs) {
+    s.row0 = rows;
+    rows += s.rows;
   }
-  out.alloc((size_t)total * W * W, ctx.stream);
-  double* o = out.get();
-  for (size_t l = 0; l < plans.size(); ++l) {
-    launch_for(ctx, W, plans[l], grids[l], o);
-    o += (int64_t)grids[l] * W * W;
-  }
-  return total;
+  const int64_t tiles = ceil_div(rows, p.B);
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(p.cap, ceil_div(tiles, tiles_per_cta)));
+  DevArray<SegDev> dsegs(segs.size(), ctx.stream);
+  FG_CUDA(cudaMemcpyAsync(dsegs.get(), segs.data(), segs.size() * sizeof(SegDev),
+                          cudaMemcpyHostToDevice, ctx.stream));
+  out.alloc((size_t)grid * W * W, ctx.stream);
+  launch_for(ctx, W, dsegs.get(), (int)segs.size(), rows, tiles, grid,
+             out.get());
+  // Pageable host -> device copies are staged before cudaMemcpyAsync
+  // returns, so `segs` may go out of scope.
+  return grid;
 }
 
 }  // namespace
@@ -305,38 +331,36 @@ void tsqr(Context& ctx, const std::vector<Span>& spans_in, int n,
     if (s.rows == 0 || s.cols == 0) continue;
     const int W = bucket(s.cols);
     DevArray<double> out;
-    TsqrSeg seg{s.data, s.rows, s.ld, s.cols, 0, 0};
-    const int cnt = factor_segments(ctx, W, {seg}, 4, out);
+    const int cnt =
+        factor(ctx, W, {SegDev{s.data, s.rows, s.ld, s.cols, 0, 0}}, 2, out);
     parts.push_back({out.get(), cnt, W, s.cols, s.col_begin});
     keep.push_back(std::move(out));
   }
 
   // Merge levels in the n-wide space until a single factor remains.
-  while (true) {
+  while (!parts.empty()) {
     int total = 0;
     for (const Partial& p : parts) total += p.count;
     if (total == 1 && parts[0].W == WN && parts[0].col_begin == 0) break;
-    if (total == 0) break;
-    std::vector<TsqrSeg> segs;
+    std::vector<SegDev> segs;
     for (const Partial& p : parts)
       for (int k = 0; k < p.count; ++k)
         segs.push_back({p.data + (int64_t)k * p.W * p.W, p.cols, p.W, p.cols,
                         p.col_begin, 0});
-    // Roughly 8 partial factors per CTA.
     DevArray<double> out;
-    const int cnt = factor_segments(ctx, WN, segs, 8, out);
+    const int cnt = factor(ctx, WN, std::move(segs), 4, out);
     parts.clear();
     parts.push_back({out.get(), cnt, WN, n, 0});
     keep.push_back(std::move(out));
   }
 
-  const int threads = 256;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(
-                                                   ceil_div((int64_t)n * n, threads), 64));
   if (parts.empty()) {
     FG_CUDA(cudaMemsetAsync(R_out, 0, sizeof(double) * n * n, ctx.stream));
     return;
   }
+  const int threads = 256;
+  const int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div((int64_t)n * n, threads), 64));
   k_normalize<<<blocks, threads, 0, ctx.stream>>>(parts[0].data, WN, n, R_out);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
