@@ -132,8 +132,11 @@ class Relation:
         self.name = name
         self.key_attrs = list(key_attrs)
         self.data_attrs = list(data_attrs)
-        self.keys = np.asarray(keys, dtype=np.int64).reshape(-1, len(self.key_attrs))
-        self.data = np.asarray(data, dtype=np.float64).reshape(-1, len(self.data_attrs))
+        data = np.asarray(data, dtype=np.float64)
+        keys = np.asarray(keys, dtype=np.int64)
+        rows = keys.shape[0] if keys.ndim and keys.shape[0] else data.shape[0] if data.ndim else 0
+        self.keys = keys.reshape(rows, len(self.key_attrs))
+        self.data = data.reshape(rows, len(self.data_attrs))
 
     @property
     def rows(self):

@@ -79,72 +79,102 @@ __device__ __forceinline__ int64_t seg_of(const int* __restrict__ begins,
 
 struct WarpSmem {
   double buf[kSmemDoubles];
-  double alpha[kMaxRB];
-  double beta[kMaxRB];
-  double hco[kMaxRB];   // head coefficient at a group's last row
-  double wt[kMaxRB];
-  int seg[kMaxRB];
-  int flags[kMaxRB];    // bit0 start, bit1 last
+  double2 coef[kMaxRB];   // {alpha, beta}: tail = a*alpha - S*beta
+  double hco[kMaxRB];     // head coefficient at a group's last row
+  double wt[kMaxRB];      // generalized weights
+  int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
+  const double* rowptr[kMaxRB];
 };
 
+// Lane geometry: the warp is split into G row-groups of L lanes; lane cl of
+// a group owns column packets cl + L*s (s < SLOTS) of VEC doubles each.
+struct Geo {
+  int vec, np, L, G;
+};
+
+template <int VEC>
+__device__ __forceinline__ void cp_async(double* dst, const double* src) {
+  __pipeline_memcpy_async(dst, src, VEC * sizeof(double));
+}
+
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
-__device__ __forceinline__ void stage_rows(const HtDev& a, WarpSmem& sm,
-                                           int64_t p, int nb, int lane) {
-  const int w = a.w;
-  const int total = nb * w;
-  for (int e = lane; e < total; e += 32) {
-    const int r = e / w;
-    const int c = e - r * w;
-    const double* src = a.data + src_row(a, p + r) * a.ld + c;
-    __pipeline_memcpy_async(&sm.buf[e], src, sizeof(double));
+template <int SLOTS, int VEC>
+__device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
+                                           WarpSmem& sm, int64_t p, int nb,
+                                           int lane) {
+  for (int rr = lane; rr < nb; rr += 32)
+    sm.rowptr[rr] = a.data + src_row(a, p + rr) * a.ld;
+  __syncwarp();
+  const int g = lane / geo.L, cl = lane % geo.L;
+  for (int rr = g; rr < nb; rr += geo.G) {
+    const double* src = sm.rowptr[rr];
+    double* dst = sm.buf + rr * a.w;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int pk = cl + geo.L * s;
+      if (pk < geo.np) cp_async<VEC>(dst + VEC * pk, src + VEC * pk);
+    }
   }
   __pipeline_commit();
 }
 
-template <int SLOTS>
-__device__ void process_unit(const HtDev& a, WarpSmem& sm, int64_t u,
-                             int lane) {
+template <int SLOTS, int VEC>
+__device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
+                             int64_t u, int lane) {
   const int w = a.w;
   const bool weighted = a.weights != nullptr;
   const int64_t p0 = u * kUnit;
   const int64_t p1 = min(p0 + kUnit, a.n_rows);
   int64_t g = seg_of(a.begins, p0, 0, a.n_seg);
+  const int grp = lane / geo.L, cl = lane % geo.L;
 
-  double S[SLOTS];
+  // Running prefix (per owned column) carried into the next batch.
+  double S[SLOTS][VEC];
 #pragma unroll
-  for (int s = 0; s < SLOTS; ++s) S[s] = 0.0;
+  for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) S[s][e] = 0.0;
   double N = 0.0;  // weighted: running sum of squared weights (lane-uniform)
 
   const int64_t gb = a.begins[g];
   if (gb < p0) {
     // The first group started in an earlier unit: get its prefix.
-    if (u > 0 && a.cont && a.cont[u - 1] == (int)g) {
-      const int V = w + (weighted ? 1 : 0);
-      const double* cr = a.carry + u * (int64_t)V;
+    const bool chained = u > 0 && a.cont && a.cont[u - 1] == (int)g;
+    const int V = w + (weighted ? 1 : 0);
+    const double* cr = chained ? a.carry + u * (int64_t)V : nullptr;
+    if (chained && weighted) N = cr[w];
 #pragma unroll
-      for (int s = 0; s < SLOTS; ++s) {
-        const int c = lane + 32 * s;
-        if (c < w) S[s] = cr[c];
-      }
-      if (weighted) N = cr[w];
-    } else {
-      for (int64_t q = gb; q < p0; ++q) {
-        const int64_t r = src_row(a, q);
-        const double v = weighted ? a.weights[r] : 1.0;
-        const double* row = a.data + r * a.ld;
+    for (int s = 0; s < SLOTS; ++s) {
+      const int pk = cl + geo.L * s;
+      if (pk >= geo.np) continue;
 #pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-          const int c = lane + 32 * s;
-          if (c < w) S[s] += weighted ? v * row[c] : row[c];
+      for (int e = 0; e < VEC; ++e) {
+        const int col = VEC * pk + e;
+        if (col >= w) continue;
+        if (chained) {
+          S[s][e] = cr[col];
+        } else {
+          double acc = 0.0;
+          for (int64_t q = gb; q < p0; ++q) {
+            const int64_t rw = src_row(a, q);
+            const double x = a.data[rw * a.ld + col];
+            acc = weighted ? fma(a.weights[rw], x, acc) : acc + x;
+          }
+          S[s][e] = acc;
         }
-        if (weighted) N += v * v;
+      }
+    }
+    if (!chained && weighted) {
+      for (int64_t q = gb; q < p0; ++q) {
+        const double v = a.weights[src_row(a, q)];
+        N = fma(v, v, N);
       }
     }
   }
 
   for (int64_t pb = p0; pb < p1; pb += a.rb) {
     const int nb = (int)(p1 - pb < (int64_t)a.rb ? p1 - pb : (int64_t)a.rb);
-    if (w > 0) stage_rows(a, sm, pb, nb, lane);
+    if (w > 0) stage_rows<SLOTS, VEC>(a, geo, sm, pb, nb, lane);
     // Row metadata and coefficients, one row per lane.
     const int64_t g_hi = (g + nb + 1 < a.n_seg) ? g + nb + 1 : a.n_seg;
     for (int base = 0; base < nb; base += 32) {
@@ -183,8 +213,7 @@ __device__ void process_unit(const HtDev& a, WarpSmem& sm, int64_t u,
         // Segmented inclusive scan of v^2 over the 32 rows of this chunk.
         double x = live ? v * v : 0.0;
         int st = live ? (fl & 1) : 0;
-        // Carry N into the first row unless it starts a group.
-        if (lane == 0 && !st) x += N;
+        if (lane == 0 && !st) x += N;  // carry unless the row starts a group
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const double y = __shfl_up_sync(0xffffffffu, x, o);
@@ -208,17 +237,14 @@ __device__ void process_unit(const HtDev& a, WarpSmem& sm, int64_t u,
           hc = 1.0 / nrm;
           sc = nrm;
         }
-        // New running N = inclusive value of the last row in this chunk.
         const int last_lane = min(31, nb - base - 1);
         N = __shfl_sync(0xffffffffu, incl, last_lane);
       }
       if (live) {
-        sm.alpha[rr] = al;
-        sm.beta[rr] = be;
+        sm.coef[rr] = make_double2(al, be);
         sm.hco[rr] = hc;
         sm.wt[rr] = v;
-        sm.seg[rr] = (int)sg;
-        sm.flags[rr] = fl;
+        sm.segfl[rr] = make_int2((int)sg, fl);
         if ((fl & 2) && a.scales) {
           const int64_t hi = a.head_index ? a.head_index[sg] : sg;
           a.scales[hi] = a.scale_count ? sqrt((double)a.scale_count[sg]) : sc;
@@ -227,42 +253,124 @@ __device__ void process_unit(const HtDev& a, WarpSmem& sm, int64_t u,
     }
     if (w > 0) __pipeline_wait_prior(0);
     __syncwarp();
-    // Column phase: each lane walks the batch rows for its columns.
-    for (int rr = 0; rr < nb; ++rr) {
-      const int fl = sm.flags[rr];
-      const int64_t sg = sm.seg[rr];
-      const double al = sm.alpha[rr];
-      const double be = sm.beta[rr];
-      const double vw = sm.wt[rr];
-      const int64_t p = pb + rr;
-      double* trow = (a.tails && !(fl & 1)) ? a.tails + (p - sg - 1) * a.ldt
-                                            : nullptr;
-      double* hrow = nullptr;
-      if ((fl & 2) && a.heads) {
-        const int64_t hi = a.head_index ? a.head_index[sg] : sg;
-        hrow = a.heads + hi * a.ldh;
-      }
-      const double hc = sm.hco[rr];
+    if (w > 0) {
+      // Rows of this batch are split into G contiguous chunks, one per
+      // row-group.  Pass 1: chunk-local sums since the last group start.
+      const int ch = (nb + geo.G - 1) / geo.G;
+      const int r_lo = min(nb, grp * ch), r_hi = min(nb, r_lo + ch);
+      double loc[SLOTS][VEC];
 #pragma unroll
-      for (int s = 0; s < SLOTS; ++s) {
-        const int c = lane + 32 * s;
-        if (c < w) {
-          if (fl & 1) S[s] = 0.0;
-          const double x = sm.buf[rr * w + c];
-          if (trow) trow[c] = x * al - S[s] * be;
-          S[s] = weighted ? fma(vw, x, S[s]) : S[s] + x;
-          if (hrow) hrow[c] = S[s] * hc;
+      for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) loc[s][e] = 0.0;
+      int has_start = 0;
+      for (int rr = r_lo; rr < r_hi; ++rr) {
+        const int fl = sm.segfl[rr].y;
+        const double vw = sm.wt[rr];
+        if (fl & 1) has_start = 1;
+        const double* row = sm.buf + rr * w;
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) {
+          const int pk = cl + geo.L * s;
+          if (pk >= geo.np) continue;
+          double x[VEC];
+          if (VEC == 2) {
+            const double2 t = *reinterpret_cast<const double2*>(row + 2 * pk);
+            x[0] = t.x;
+            x[VEC - 1] = t.y;
+          } else {
+            x[0] = row[pk];
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double base_ = (fl & 1) ? 0.0 : loc[s][e];
+            loc[s][e] = weighted ? fma(vw, x[e], base_) : base_ + x[e];
+          }
+        }
+      }
+      // Pass 2: segmented scan of the chunk sums across the G groups,
+      // seeded with the batch carry S.
+      int f = has_start;
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          if (grp == 0 && !f) loc[s][e] += S[s][e];
+      for (int o = 1; o < geo.G; o <<= 1) {
+        const int fy = __shfl_up_sync(0xffffffffu, f, o * geo.L);
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double y = __shfl_up_sync(0xffffffffu, loc[s][e], o * geo.L);
+            if (grp >= o && !f) loc[s][e] += y;
+          }
+        if (grp >= o) f |= fy;
+      }
+      double run[SLOTS][VEC];
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const double ex = __shfl_up_sync(0xffffffffu, loc[s][e], geo.L);
+          run[s][e] = grp == 0 ? S[s][e] : ex;
+          S[s][e] = __shfl_sync(0xffffffffu, loc[s][e], (geo.G - 1) * geo.L + cl);
+        }
+      // Pass 3: emit tails (and heads at group ends) for this chunk.
+      for (int rr = r_lo; rr < r_hi; ++rr) {
+        const int2 sf = sm.segfl[rr];
+        const double2 cf = sm.coef[rr];
+        const double vw = sm.wt[rr];
+        const int64_t p = pb + rr;
+        double* trow = (a.tails && !(sf.y & 1)) ? a.tails + (p - sf.x - 1) * a.ldt
+                                               : nullptr;
+        double* hrow = nullptr;
+        double hc = 0.0;
+        if ((sf.y & 2) && a.heads) {
+          const int64_t hi = a.head_index ? a.head_index[sf.x] : sf.x;
+          hrow = a.heads + hi * a.ldh;
+          hc = sm.hco[rr];
+        }
+        const double* row = sm.buf + rr * w;
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) {
+          const int pk = cl + geo.L * s;
+          if (pk >= geo.np) continue;
+          double x[VEC], o[VEC];
+          if (VEC == 2) {
+            const double2 t = *reinterpret_cast<const double2*>(row + 2 * pk);
+            x[0] = t.x;
+            x[VEC - 1] = t.y;
+          } else {
+            x[0] = row[pk];
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            if (sf.y & 1) run[s][e] = 0.0;
+            o[e] = x[e] * cf.x - run[s][e] * cf.y;
+            run[s][e] = weighted ? fma(vw, x[e], run[s][e]) : run[s][e] + x[e];
+          }
+          if (trow) {
+            if (VEC == 2)
+              *reinterpret_cast<double2*>(trow + 2 * pk) = make_double2(o[0], o[VEC - 1]);
+            else
+              trow[pk] = o[0];
+          }
+          if (hrow) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) hrow[VEC * pk + e] = run[s][e] * hc;
+          }
         }
       }
     }
-    g = sm.seg[nb - 1];
+    g = sm.segfl[nb - 1].x;
     __syncwarp();
   }
 }
 
-template <int SLOTS>
+template <int SLOTS, int VEC>
 __global__ void __launch_bounds__(kWarps * 32)
-    k_heads_tails(HtDev a) {
+    k_heads_tails(HtDev a, Geo geo) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem* all = reinterpret_cast<WarpSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -273,7 +381,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     if (lane == 0) u = atomicAdd(a.ticket, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= a.n_units) break;
-    process_unit<SLOTS>(a, sm, u, lane);
+    process_unit<SLOTS, VEC>(a, geo, sm, u, lane);
   }
 }
 
@@ -370,27 +478,33 @@ __global__ void k_join(JoinArgs a) {
   }
 }
 
-template <int SLOTS>
-void launch_main(Context& ctx, const HtDev& d) {
+template <int SLOTS, int VEC>
+void launch_main(Context& ctx, const HtDev& d, const Geo& geo) {
   const size_t smem = sizeof(WarpSmem) * kWarps;
-  static bool configured = false;
-  if (!configured) {
-    FG_CUDA(cudaFuncSetAttribute(k_heads_tails<SLOTS>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    configured = true;
-  }
+  auto kern = k_heads_tails<SLOTS, VEC>;
+  FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
   int per_sm = 0;
-  FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, k_heads_tails<SLOTS>, kWarps * 32, smem));
+  FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                        kWarps * 32, smem));
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)ctx.sm_count * per_sm;
   const int64_t need = ceil_div(d.n_units, kWarps);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k_heads_tails<SLOTS><<<(int)grid, kWarps * 32, smem, ctx.stream>>>(d);
+  kern<<<(int)grid, kWarps * 32, smem, ctx.stream>>>(d, geo);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
+}
+
+template <int VEC>
+void launch_slots(Context& ctx, const HtDev& d, const Geo& geo) {
+  const int slots = (geo.np + geo.L - 1) / geo.L;
+  if (slots <= 1) launch_main<1, VEC>(ctx, d, geo);
+  else if (slots <= 2) launch_main<2, VEC>(ctx, d, geo);
+  else if (slots <= 4) launch_main<4, VEC>(ctx, d, geo);
+  else if (slots <= 8) launch_main<8, VEC>(ctx, d, geo);
+  else launch_main<16, VEC>(ctx, d, geo);
 }
 
 }  // namespace
@@ -441,12 +555,24 @@ void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
     d.cont = cont.get();
     d.carry = carry.get();
   }
-  const int slots = (in.w + 31) / 32;
-  if (slots <= 1) launch_main<1>(ctx, d);
-  else if (slots <= 2) launch_main<2>(ctx, d);
-  else if (slots <= 4) launch_main<4>(ctx, d);
-  else if (slots <= 8) launch_main<8>(ctx, d);
-  else launch_main<32>(ctx, d);
+  // Vector width, lanes per row-group and rows per batch.
+  Geo geo{};
+  const bool aligned = in.w > 0 && in.w % 2 == 0 && in.ld % 2 == 0 &&
+                       (reinterpret_cast<uintptr_t>(in.data) % 16 == 0) &&
+                       (!in.tails || (in.ldt % 2 == 0 &&
+                                      reinterpret_cast<uintptr_t>(in.tails) % 16 == 0));
+  geo.vec = aligned ? 2 : 1;
+  geo.np = in.w > 0 ? (in.w + geo.vec - 1) / geo.vec : 1;
+  geo.L = 1;
+  while (geo.L < geo.np && geo.L < 32) geo.L <<= 1;
+  geo.G = 32 / geo.L;
+  if (in.w > 0) {
+    int rb = std::min(kMaxRB, kSmemDoubles / in.w);
+    if (rb >= geo.G) rb -= rb % geo.G;
+    d.rb = std::max(1, rb);
+  }
+  if (geo.vec == 2) launch_slots<2>(ctx, d, geo);
+  else launch_slots<1>(ctx, d, geo);
 }
 
 void launch_join(Context& ctx, const JoinArgs& a) {

@@ -206,6 +206,139 @@ __global__ void __launch_bounds__(C::NT)
   for (int e = threadIdx.x; e < C::W * C::W; e += C::NT) o[e] = R[e];
 }
 
+// ---------------------------------------------------------------------------
+// Warp-level variant for W <= 32: every warp owns its own accumulator R
+// (shared memory, W x W) and absorbs B = TR*RPT-row tiles with warp
+// shuffles only -- no CTA barriers.  The column loop is fully unrolled, the
+// pivot column is broadcast to all lanes so the reflector is computed
+// redundantly without divergence, and each lane forms v for its own rows.
+// Partial factors are one per warp.
+
+template <int W_, int TR_, int RPT_>
+struct WCfg {
+  static constexpr int W = W_;
+  static constexpr int CPT = W >= 8 ? 2 : 1;
+  static constexpr int TC = W / CPT;
+  static constexpr int TR = TR_;
+  static constexpr int RPT = RPT_;
+  static constexpr int B = TR * RPT;
+  static constexpr int WARPS = 8;
+  static constexpr int NT = 32 * WARPS;
+  static constexpr size_t smem_bytes = sizeof(double) * W * W * WARPS;
+  static_assert(TC * TR == 32, "TC * TR must be a warp");
+};
+
+template <class C>
+__device__ __forceinline__ int wcol(int q, int c) {
+  return (q & 1) ? (q + 1) * C::TC - 1 - c : q * C::TC + c;
+}
+
+template <class C>
+__device__ __forceinline__ double wgroup_sum(double x) {
+#pragma unroll
+  for (int o = C::TR / 2; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT)
+    k_tsqr_warp(const SegDev* __restrict__ segs, int nseg, int64_t total_rows,
+                int64_t total_tiles, double* __restrict__ out) {
+  extern __shared__ __align__(16) double wsm[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  double* R = wsm + wib * C::W * C::W;
+  const int r = lane % C::TR;
+  const int c = lane / C::TR;
+  for (int e = lane; e < C::W * C::W; e += 32) R[e] = 0.0;
+  __syncwarp();
+  int cols[C::CPT];
+#pragma unroll
+  for (int q = 0; q < C::CPT; ++q) cols[q] = wcol<C>(q, c);
+  const int64_t gw = (int64_t)blockIdx.x * C::WARPS + wib;
+  const int64_t nw = (int64_t)gridDim.x * C::WARPS;
+
+  for (int64_t t = gw; t < total_tiles; t += nw) {
+    double X[C::RPT][C::CPT];
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i) {
+      const int64_t gr = t * C::B + i * C::TR + r;
+      const double* rp = nullptr;
+      int lo = 0, hi = 0;
+      if (gr < total_rows) {
+        int s = 0;
+        if (nseg > 1) {
+          int a = 0, b = nseg;
+          while (b - a > 1) {
+            const int mid = (a + b) >> 1;
+            if (segs[mid].row0 <= gr) a = mid; else b = mid;
+          }
+          s = a;
+        }
+        const SegDev& sg = segs[s];
+        rp = sg.data + (gr - sg.row0) * sg.ld - sg.col_begin;
+        lo = sg.col_begin;
+        hi = sg.col_begin + sg.cols;
+      }
+#pragma unroll
+      for (int q = 0; q < C::CPT; ++q)
+        X[i][q] = (rp && cols[q] >= lo && cols[q] < hi) ? __ldg(rp + cols[q]) : 0.0;
+    }
+
+#pragma unroll
+    for (int k = 0; k < C::W; ++k) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int qb = k / C::TC;
+      const int within = k % C::TC;
+      const int ck = (qb & 1) ? C::TC - 1 - within : within;
+      // Pivot column to every lane (same rows r), then the reflector.
+      double v[C::RPT];
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < C::RPT; ++i) {
+        v[i] = __shfl_sync(0xffffffffu, X[i][qb], r + ck * C::TR);
+        if (i & 1) s1 = fma(v[i], v[i], s1); else s0 = fma(v[i], v[i], s0);
+      }
+      const double sig = wgroup_sum<C>(s0 + s1);
+      const double alpha = R[k * C::W + k];
+      if (!(sig > 0.0)) continue;  // warp-uniform: H = I
+      const double nrm = sqrt(fma(alpha, alpha, sig));
+      const double beta = alpha >= 0.0 ? -nrm : nrm;
+      const double u = alpha - beta;
+      const double inv = 1.0 / (u * beta);
+      const double tau = -u * u * inv;   // (beta - alpha) / beta
+      const double scal = beta * inv;    // 1 / (alpha - beta)
+#pragma unroll
+      for (int i = 0; i < C::RPT; ++i) v[i] *= scal;
+#pragma unroll
+      for (int q = qb; q < C::CPT; ++q) {
+        const int j = cols[q];
+        const bool act = j > k;
+        const double rkj = R[k * C::W + j];
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < C::RPT; ++i) {
+          if (i & 1) d1 = fma(v[i], X[i][q], d1); else d0 = fma(v[i], X[i][q], d0);
+        }
+        const double f = tau * (wgroup_sum<C>(d0 + d1) + rkj);
+        if (act) {
+#pragma unroll
+          for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
+        }
+        __syncwarp();
+        if (act && r == 0) R[k * C::W + j] = rkj - f;
+      }
+      __syncwarp();
+      if (lane == 0) R[k * C::W + k] = beta;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  double* o = out + gw * C::W * C::W;
+  for (int e = lane; e < C::W * C::W; e += 32) o[e] = R[e];
+}
+
 __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
                             double* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n;
@@ -217,12 +350,12 @@ __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
   }
 }
 
-using C4 = Cfg<4, 4, 32, 8>;
-using C8 = Cfg<8, 4, 32, 8>;
-using C16 = Cfg<16, 8, 16, 16>;
-using C32 = Cfg<32, 16, 16, 8>;
 using C64 = Cfg<64, 32, 8, 16>;
 using C128 = Cfg<128, 32, 8, 8>;
+using W4 = WCfg<4, 8, 8>;
+using W8 = WCfg<8, 8, 8>;
+using W16 = WCfg<16, 4, 16>;
+using W32 = WCfg<32, 2, 16>;
 
 int bucket(int w) {
   for (int b : {4, 8, 16, 32, 64, 128})
@@ -230,57 +363,56 @@ int bucket(int w) {
   return 0;
 }
 
-template <class C>
-int max_ctas(Context& ctx) {
-  FG_CUDA(cudaFuncSetAttribute(k_tsqr<C>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)C::smem_bytes));
-  int per_sm = 0;
-  FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsqr<C>,
-                                                        C::NT, C::smem_bytes));
-  return std::max(1, per_sm) * ctx.sm_count;
-}
-
+// Launch shape of one factorisation kernel: rows per tile, partial factors
+// per CTA, and the resident-CTA cap.
 struct Plan {
   int B;
+  int per_cta;
   int cap;
 };
 
+template <class K>
+int resident(Context& ctx, K kern, int nt, size_t smem) {
+  FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  int per_sm = 0;
+  FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
+  return std::max(1, per_sm) * ctx.sm_count;
+}
+
 template <class C>
-Plan plan_of(Context& ctx) {
-  return {C::B, max_ctas<C>(ctx)};
+Plan plan_cta(Context& ctx) {
+  return {C::B, 1, resident(ctx, k_tsqr<C>, C::NT, C::smem_bytes)};
+}
+template <class C>
+Plan plan_warp(Context& ctx) {
+  return {C::B, C::WARPS, resident(ctx, k_tsqr_warp<C>, C::NT, C::smem_bytes)};
 }
 
 Plan plan_for(Context& ctx, int W) {
   switch (W) {
-    case 4: return plan_of<C4>(ctx);
-    case 8: return plan_of<C8>(ctx);
-    case 16: return plan_of<C16>(ctx);
-    case 32: return plan_of<C32>(ctx);
-    case 64: return plan_of<C64>(ctx);
-    default: return plan_of<C128>(ctx);
+    case 4: return plan_warp<W4>(ctx);
+    case 8: return plan_warp<W8>(ctx);
+    case 16: return plan_warp<W16>(ctx);
+    case 32: return plan_warp<W32>(ctx);
+    case 64: return plan_cta<C64>(ctx);
+    default: return plan_cta<C128>(ctx);
   }
-}
-
-template <class C>
-void launch(Context& ctx, const SegDev* segs, int nseg, int64_t rows,
-            int64_t tiles, int grid, double* out) {
-  k_tsqr<C><<<grid, C::NT, C::smem_bytes, ctx.stream>>>(segs, nseg, rows,
-                                                         tiles, out);
-  FG_LAUNCHED(ctx);
-  FG_KERNEL_CHECK();
 }
 
 void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
                 int64_t rows, int64_t tiles, int grid, double* out) {
+  cudaStream_t s = ctx.stream;
   switch (W) {
-    case 4: launch<C4>(ctx, segs, nseg, rows, tiles, grid, out); break;
-    case 8: launch<C8>(ctx, segs, nseg, rows, tiles, grid, out); break;
-    case 16: launch<C16>(ctx, segs, nseg, rows, tiles, grid, out); break;
-    case 32: launch<C32>(ctx, segs, nseg, rows, tiles, grid, out); break;
-    case 64: launch<C64>(ctx, segs, nseg, rows, tiles, grid, out); break;
-    default: launch<C128>(ctx, segs, nseg, rows, tiles, grid, out); break;
+    case 4: k_tsqr_warp<W4><<<grid, W4::NT, W4::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
+    case 8: k_tsqr_warp<W8><<<grid, W8::NT, W8::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
+    case 16: k_tsqr_warp<W16><<<grid, W16::NT, W16::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
+    case 32: k_tsqr_warp<W32><<<grid, W32::NT, W32::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
+    case 64: k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
+    default: k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
   }
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
 }
 
 // A batch of W x W partial factors, meaningful width `cols` at `col_begin`.
@@ -292,9 +424,10 @@ struct Partial {
   int col_begin;
 };
 
-// Factors the concatenation of `segs` (bucket W) with CTAs taking about
-// `tiles_per_cta` tiles each; returns the number of partial factors in out.
-int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_cta,
+// Factors the concatenation of `segs` (bucket W); each factor unit (CTA or
+// warp) takes about `tiles_per_unit` tiles.  Returns the number of partial
+// factors written to out.
+int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_unit,
            DevArray<double>& out) {
   const Plan p = plan_for(ctx, W);
   int64_t rows = 0;
@@ -304,16 +437,16 @@ int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_cta,
   }
   const int64_t tiles = ceil_div(rows, p.B);
   const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(p.cap, ceil_div(tiles, tiles_per_cta)));
+      1, std::min<int64_t>(p.cap, ceil_div(tiles, tiles_per_unit * p.per_cta)));
   DevArray<SegDev> dsegs(segs.size(), ctx.stream);
   FG_CUDA(cudaMemcpyAsync(dsegs.get(), segs.data(), segs.size() * sizeof(SegDev),
                           cudaMemcpyHostToDevice, ctx.stream));
-  out.alloc((size_t)grid * W * W, ctx.stream);
-  launch_for(ctx, W, dsegs.get(), (int)segs.size(), rows, tiles, grid,
-             out.get());
+  const int units = grid * p.per_cta;
+  out.alloc((size_t)units * W * W, ctx.stream);
+  launch_for(ctx, W, dsegs.get(), (int)segs.size(), rows, tiles, grid, out.get());
   // Pageable host -> device copies are staged before cudaMemcpyAsync
   // returns, so `segs` may go out of scope.
-  return grid;
+  return units;
 }
 
 }  // namespace

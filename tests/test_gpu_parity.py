@@ -1,0 +1,231 @@
+"""Pipeline parity on the GPU through the C ABI against the compiled reference.
+
+Bars (BASELINE.json north_star): segment offsets, keys and all six count
+tables bit-exact; R within relative Frobenius 1e-10 after sign normalisation
+(rank-deficient references compare R^T R, since R is then not unique).
+Sources of truth: tests/golden (written by oracle/_ref/figaro_ref) and, when
+the binary is present, fresh runs of oracle/_ref/figaro_ref on seeded inputs.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import figaro_np as fo  # noqa: E402
+from paper_2204_00525_b200 import fgdb, workloads  # noqa: E402
+from paper_2204_00525_b200 import figaro as F  # noqa: E402
+from tests.conftest import REF_BIN, golden  # noqa: E402
+from tests.helpers import golden_stems, r_distance  # noqa: E402
+
+R_TOL = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def to_rels(db, device=True, canonical=False):
+    out = []
+    for r in db.relations:
+        keys, data = r.keys, r.data
+        if canonical:
+            c = fo.canonicalize(fo.Relation(r.name, r.key_attrs, r.data_attrs, keys, data))
+            keys, data = c.keys, c.data
+        if device:
+            keys, data = torch.from_numpy(np.ascontiguousarray(keys)).cuda(), \
+                torch.from_numpy(np.ascontiguousarray(data)).cuda()
+        out.append(F.Relation(r.name, r.key_attrs, r.data_attrs, keys, data))
+    return out
+
+
+def run_gpu(db, device=True, canonical=False, keep_r0=False, assume_reduced=True):
+    rels = to_rels(db, device, canonical)
+    tree = F.build_join_tree(rels, db.root, db.parent)
+    res = F.run_pipeline(rels, tree, F.PipelineOptions(assume_reduced=assume_reduced),
+                         keep_r0=keep_r0)
+    R = res.factor.r.cpu().numpy() if device else res.factor.r
+    return res, R
+
+
+def check_counts(res, ref):
+    for i, nc in enumerate(ref.nodes):
+        c = res.counts[i]
+        assert np.array_equal(c.group_begin.astype(np.uint64), nc.group_begin), f"segments node {i}"
+        assert np.array_equal(c.keys, nc.keys), f"keys node {i}"
+        for name in ("rows_per_key", "theta_down", "full_join_size", "phi_circ", "phi_down", "phi_up"):
+            assert np.array_equal(getattr(c, name), getattr(nc, name)), f"{name} node {i}"
+        assert np.array_equal(c.parent_keys, nc.pkeys), f"parent keys node {i}"
+
+
+def match_r0(spans, ref_blocks):
+    """Each GPU span equals the vertical concatenation of the next
+    reference OutBlocks with the same node / col_begin."""
+    it = iter(ref_blocks)
+    for sp in spans:
+        rows = []
+        got = 0
+        while got < sp.rows.shape[0]:
+            b = next(it)
+            assert (b.node, b.col_begin, b.rows.shape[1]) == (sp.node, sp.col_begin, sp.rows.shape[1])
+            rows.append(b.rows)
+            got += b.rows.shape[0]
+        ref = np.vstack(rows)
+        scale = max(np.abs(ref).max(), 1e-300)
+        np.testing.assert_allclose(sp.rows, ref, rtol=0, atol=1e-12 * scale)
+    assert next(it, None) is None
+
+
+GOLD = golden_stems("rnd_") + golden_stems("hand_") + golden_stems("big_")
+
+
+@pytest.mark.parametrize("stem", GOLD)
+@pytest.mark.parametrize("device", [True, False])
+def test_golden_pipeline(stem, device):
+    db = fgdb.read_fgdb(golden(stem + ".fgdb"))
+    ref = fgdb.read_fgrs(golden(stem + ".fgrs"))
+    res, R = run_gpu(db, device=device)
+    assert res.r0_rows == ref.r0_rows and res.input_rows == ref.input_rows
+    assert r_distance(R, ref.R) <= R_TOL
+    check_counts(res, ref)
+    if os.path.exists(golden(stem + ".fgrm")):
+        assert r_distance(R, fgdb.read_fgrm(golden(stem + ".fgrm"))) <= R_TOL
+
+
+@pytest.mark.parametrize("stem", GOLD)
+def test_golden_r0_elementwise(stem):
+    """With canonically pre-sorted input the R0 spans equal the reference
+    blocks element-wise (figaro.hpp:166-329 block order)."""
+    db = fgdb.read_fgdb(golden(stem + ".fgdb"))
+    ref = fgdb.read_fgrs(golden(stem + ".fgrs"))
+    res, _ = run_gpu(db, canonical=True, keep_r0=True)
+    match_r0(res.r0, ref.r0)
+
+
+def test_ground_truth_accuracy():
+    # acceptance criterion 6: <= 5e-14 at 512x16 against the fixed factor
+    for stem in ("gt_512x16", "gt_64x8"):
+        db = fgdb.read_fgdb(golden(stem + ".fgdb"))
+        rfix = fgdb.read_fgrm(golden(stem + ".rfix.fgrm"))
+        _, R = run_gpu(db)
+        n = rfix.shape[0]
+        assert fo.rel_frobenius_distance(fo.normalize_signs(R[:n, :n]), fo.normalize_signs(rfix)) <= 5e-14
+
+
+def test_c1_full_golden():
+    db = workloads.config_c1(seed=7)
+    ref = fgdb.read_fgrs(golden("c1_seed7.fgrs"))
+    res, R = run_gpu(db)
+    assert r_distance(R, ref.R) <= R_TOL
+    check_counts(res, ref)
+
+
+def run_ref(db, tmp_path, extra=()):
+    p = str(tmp_path / "db.fgdb")
+    fgdb.write_fgdb(p, db)
+    subprocess.run([REF_BIN, "run", p, p + ".rs", *extra], check=True, capture_output=True)
+    return fgdb.read_fgrs(p + ".rs")
+
+
+@pytest.mark.parametrize("cfg,scale", [("C2", 0.01), ("C3", 0.002), ("C4", 0.02), ("C5", 0.005)])
+def test_configs_vs_reference(cfg, scale, tmp_path, ref_bin):
+    db = workloads.make(cfg, seed=11, scale=scale)
+    ref = run_ref(db, tmp_path)
+    res, R = run_gpu(db)
+    assert res.r0_rows == ref.r0_rows
+    assert r_distance(R, ref.R) <= R_TOL
+    check_counts(res, ref)
+
+
+@pytest.mark.parametrize("seed", range(200, 215))
+def test_random_reference_databases(seed, tmp_path, ref_bin):
+    p = str(tmp_path / "rnd.fgdb")
+    subprocess.run([ref_bin, "random", str(seed), p, "--max-rows", "2000", "--max-rel", "6",
+                    "--key-domain", "30", "--max-cols", "14"], check=True, capture_output=True)
+    db = fgdb.read_fgdb(p)
+    ref = run_ref(db, tmp_path)
+    res, R = run_gpu(db)
+    assert r_distance(R, ref.R) <= R_TOL
+    check_counts(res, ref)
+
+
+def test_unreduced_input_is_reduced(tmp_path, ref_bin):
+    """assume_reduced=False runs the semi-join reducer (reduce.hpp:47-74)."""
+    db = workloads.make("C5", seed=3, scale=0.002)
+    rng = np.random.default_rng(0)
+    for r in db.relations:  # dangling keys on both sides
+        extra = rng.integers(200_000, 200_050, 40).reshape(-1, 1)
+        r.keys = np.vstack([r.keys, extra])
+        r.data = np.vstack([r.data, rng.standard_normal((40, r.data.shape[1]))])
+    ref = run_ref(db, tmp_path, ["--reduce"])
+    res, R = run_gpu(db, assume_reduced=False)
+    assert res.input_rows == ref.input_rows
+    assert r_distance(R, ref.R) <= R_TOL
+    check_counts(res, ref)
+    with pytest.raises(F.integrity_error):
+        run_gpu(db, assume_reduced=True)
+
+
+def test_errors_match_reference_taxonomy():
+    mk = fgdb.RelationData
+    k = lambda *v: np.array(v, dtype=np.int64).reshape(-1, 1)  # noqa: E731
+    d = lambda n: np.ones((n, 1))  # noqa: E731
+    # unreduced (counts.hpp:143-148 / 211-214)
+    for a, b in ((k(1, 2), k(1)), (k(1), k(1, 2))):
+        db = fgdb.Database([mk("S", ["X"], ["a"], a, d(len(a))), mk("T", ["X"], ["b"], b, d(len(b)))], 0, [-1, 0])
+        with pytest.raises(F.integrity_error):
+            run_gpu(db)
+    # 300^8 > 2^64 (counts.hpp:47-62)
+    rels = [mk(f"S{i}", ["X"], [f"y{i}"], np.ones((300, 1), dtype=np.int64),
+               np.arange(300.0).reshape(300, 1)) for i in range(8)]
+    with pytest.raises(F.size_error):
+        run_gpu(fgdb.Database(rels, 0, [-1] + [0] * 7))
+    # empty join after reduction (reduce.hpp:49-53)
+    db = fgdb.Database([mk("S", ["X"], ["a"], k(1), d(1)), mk("T", ["X"], ["b"], k(2), d(1))], 0, [-1, 0])
+    with pytest.raises(F.empty_join_error):
+        run_gpu(db, assume_reduced=False)
+    # tree errors (join_tree.hpp:72-180)
+    db = fgdb.Database([mk("S", ["X"], ["a"], k(1), d(1)), mk("T", ["Y"], ["b"], k(1), d(1))], 0, [-1, 0])
+    with pytest.raises(F.tree_error):
+        run_gpu(db)
+    db = fgdb.Database([mk("S", ["X"], ["a"], k(1), d(1)), mk("T", ["X"], ["a"], k(1), d(1))], 0, [-1, 0])
+    with pytest.raises(F.schema_error):
+        run_gpu(db)
+
+
+def test_determinism_and_launch_evidence():
+    db = workloads.make("C5", seed=5, scale=0.003)
+    r1, R1 = run_gpu(db)
+    r2, R2 = run_gpu(db)
+    assert np.array_equal(R1, R2), "R must be bit-identical run to run"
+    assert r1.kernels > 10
+
+
+def test_full_size_c2_gram_property():
+    """BASELINE-size C2 (32M rows): R^T R equals the join's A^T A computed
+    independently from per-key sums (size-independent property)."""
+    db = workloads.config_c2(seed=7)
+    res, R = run_gpu(db)
+    assert res.input_rows == 32_000_000 and res.r0_rows == 31_000_000
+    for c in res.counts:
+        assert np.all(c.rows_per_key == 16) and np.all(c.phi_circ == 16)
+    ata = np.zeros((32, 32))
+    blocks = []
+    for r in db.relations:
+        k = torch.from_numpy(r.keys[:, 0]).cuda()
+        x = torch.from_numpy(r.data).cuda()
+        sums = torch.zeros((1_000_000, 16), dtype=torch.float64, device="cuda").index_add_(0, k, x)
+        blocks.append((x, sums))
+    (x1, s1), (x2, s2) = blocks
+    ata[:16, :16] = (16 * (x1.T @ x1)).cpu().numpy()
+    ata[16:, 16:] = (16 * (x2.T @ x2)).cpu().numpy()
+    cross = (s1.T @ s2).cpu().numpy()
+    ata[:16, 16:] = cross
+    ata[16:, :16] = cross.T
+    assert fo.rel_frobenius_distance(R.T @ R, ata) <= 1e-12
