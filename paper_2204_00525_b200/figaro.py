@@ -143,12 +143,18 @@ class Relation:
     data: object
 
     def __post_init__(self):
+        rows = None
+        for x in (self.keys, self.data):
+            if getattr(x, "ndim", 0) == 2:
+                rows = int(x.shape[0])
         if not _is_torch(self.keys):
-            self.keys = np.ascontiguousarray(np.asarray(self.keys, dtype=np.int64)
-                                             .reshape(-1, len(self.key_attrs)))
+            k = np.asarray(self.keys, dtype=np.int64)
+            self.keys = np.ascontiguousarray(
+                k.reshape(rows if rows is not None else -1, len(self.key_attrs)))
         if not _is_torch(self.data):
-            self.data = np.ascontiguousarray(np.asarray(self.data, dtype=np.float64)
-                                             .reshape(-1, len(self.data_attrs)))
+            d = np.asarray(self.data, dtype=np.float64)
+            self.data = np.ascontiguousarray(
+                d.reshape(rows if rows is not None else -1, len(self.data_attrs)))
 
     def row_count(self) -> int:
         return int(self.keys.shape[0])
