@@ -112,7 +112,7 @@ __device__ __forceinline__ void stage_tile(const SegDev* __restrict__ segs,
 template <class C>
 __global__ void __launch_bounds__(C::NT)
     k_tsqr(const SegDev* __restrict__ segs, int nseg, int64_t total_rows,
-           int64_t total_tiles, double* __restrict__ out) {
+           int64_t total_tiles, int64_t nunits, double* __restrict__ out) {
   extern __shared__ __align__(16) double sm[];
   double* R = sm;                         // W x W
   double* vbuf = R + C::W * C::W;         // 2 x B
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(C::NT)
   int64_t t = blockIdx.x;
   if (t < total_tiles) stage_tile<C>(segs, nseg, total_rows, t, stage, rowseg);
 
-  for (; t < total_tiles; t += gridDim.x) {
+  for (; t < total_tiles; t += nunits) {
     __pipeline_wait_prior(0);
     __syncthreads();
 #pragma unroll
@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(C::NT)
       for (int q = 0; q < C::CPT; ++q)
         X[i][q] = stage[(i * C::TR + r) * C::LDS + col_of<C>(q, c)];
     __syncthreads();
-    if (t + gridDim.x < total_tiles)
-      stage_tile<C>(segs, nseg, total_rows, t + gridDim.x, stage, rowseg);
+    if (t + nunits < total_tiles)
+      stage_tile<C>(segs, nseg, total_rows, t + nunits, stage, rowseg);
 
 #pragma unroll
     for (int qb = 0; qb < C::CPT; ++qb) {
@@ -243,7 +243,7 @@ __device__ __forceinline__ double wgroup_sum(double x) {
 template <class C>
 __global__ void __launch_bounds__(C::NT)
     k_tsqr_warp(const SegDev* __restrict__ segs, int nseg, int64_t total_rows,
-                int64_t total_tiles, double* __restrict__ out) {
+                int64_t total_tiles, int64_t nunits, double* __restrict__ out) {
   extern __shared__ __align__(16) double wsm[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(C::NT)
 #pragma unroll
   for (int q = 0; q < C::CPT; ++q) cols[q] = wcol<C>(q, c);
   const int64_t gw = (int64_t)blockIdx.x * C::WARPS + wib;
-  const int64_t nw = (int64_t)gridDim.x * C::WARPS;
+  const int64_t nw = nunits;
+  if (gw >= nunits) return;
 
   for (int64_t t = gw; t < total_tiles; t += nw) {
     double X[C::RPT][C::CPT];
@@ -401,15 +402,15 @@ Plan plan_for(Context& ctx, int W) {
 }
 
 void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
-                int64_t rows, int64_t tiles, int grid, double* out) {
+                int64_t rows, int64_t tiles, int64_t units, int grid, double* out) {
   cudaStream_t s = ctx.stream;
   switch (W) {
-    case 4: k_tsqr_warp<W4><<<grid, W4::NT, W4::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
-    case 8: k_tsqr_warp<W8><<<grid, W8::NT, W8::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
-    case 16: k_tsqr_warp<W16><<<grid, W16::NT, W16::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
-    case 32: k_tsqr_warp<W32><<<grid, W32::NT, W32::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
-    case 64: k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
-    default: k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, out); break;
+    case 4: k_tsqr_warp<W4><<<grid, W4::NT, W4::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 8: k_tsqr_warp<W8><<<grid, W8::NT, W8::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 16: k_tsqr_warp<W16><<<grid, W16::NT, W16::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 32: k_tsqr_warp<W32><<<grid, W32::NT, W32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 64: k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    default: k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
   }
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
@@ -436,17 +437,17 @@ int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_unit
     rows += s.rows;
   }
   const int64_t tiles = ceil_div(rows, p.B);
-  const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(p.cap, ceil_div(tiles, tiles_per_unit * p.per_cta)));
+  const int64_t units = std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)p.cap * p.per_cta, ceil_div(tiles, tiles_per_unit)));
+  const int grid = (int)ceil_div(units, p.per_cta);
   DevArray<SegDev> dsegs(segs.size(), ctx.stream);
   FG_CUDA(cudaMemcpyAsync(dsegs.get(), segs.data(), segs.size() * sizeof(SegDev),
                           cudaMemcpyHostToDevice, ctx.stream));
-  const int units = grid * p.per_cta;
   out.alloc((size_t)units * W * W, ctx.stream);
-  launch_for(ctx, W, dsegs.get(), (int)segs.size(), rows, tiles, grid, out.get());
+  launch_for(ctx, W, dsegs.get(), (int)segs.size(), rows, tiles, units, grid, out.get());
   // Pageable host -> device copies are staged before cudaMemcpyAsync
-  // returns, so `segs` may go out of scope.
-  return units;
+  // returns, so `segs` may go out of scope.  Every unit gets >= 1 tile.
+  return (int)units;
 }
 
 }  // namespace
@@ -482,6 +483,8 @@ void tsqr(Context& ctx, const std::vector<Span>& spans_in, int n,
                         p.col_begin, 0});
     DevArray<double> out;
     const int cnt = factor(ctx, WN, std::move(segs), 4, out);
+    if (cnt >= total && total > 1)
+      fail(FG_E_CUDA, "TSQR merge level did not reduce the number of factors");
     parts.clear();
     parts.push_back({out.get(), cnt, WN, n, 0});
     keep.push_back(std::move(out));
