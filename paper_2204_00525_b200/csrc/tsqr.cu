@@ -23,6 +23,8 @@
 #include <cuda_pipeline.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "launchers.cuh"
 
@@ -214,17 +216,19 @@ __global__ void __launch_bounds__(C::NT)
 // redundantly without divergence, and each lane forms v for its own rows.
 // Partial factors are one per warp.
 
-template <int W_, int TR_, int RPT_>
+template <int W_, int CPT_, int RPT_, int MINB_ = 1>
 struct WCfg {
   static constexpr int W = W_;
-  static constexpr int CPT = W >= 8 ? 2 : 1;
+  static constexpr int CPT = CPT_;
   static constexpr int TC = W / CPT;
-  static constexpr int TR = TR_;
+  static constexpr int TR = 32 / TC;
   static constexpr int RPT = RPT_;
   static constexpr int B = TR * RPT;
+  static constexpr int RR = (W + TR - 1) / TR;  // accumulator rows per lane
   static constexpr int WARPS = 8;
   static constexpr int NT = 32 * WARPS;
-  static constexpr size_t smem_bytes = sizeof(double) * W * W * WARPS;
+  static constexpr int MINB = MINB_;
+  static constexpr size_t smem_bytes = 0;
   static_assert(TC * TR == 32, "TC * TR must be a warp");
 };
 
@@ -240,26 +244,31 @@ __device__ __forceinline__ double wgroup_sum(double x) {
   return x;
 }
 
+// Lane (r, c) holds tile rows i*TR + r (i < RPT) of its CPT columns and the
+// accumulator entries R[m*TR + r][col] (m < RR) of the same columns, so the
+// whole column loop is straight-line register code: pivot broadcast by
+// shuffle, reflector computed redundantly by every lane (branch-free, tau = 0
+// for an all-zero column), dot products reduced over the TR row lanes.
 template <class C>
-__global__ void __launch_bounds__(C::NT)
+__global__ void __launch_bounds__(C::NT, C::MINB)
     k_tsqr_warp(const SegDev* __restrict__ segs, int nseg, int64_t total_rows,
                 int64_t total_tiles, int64_t nunits, double* __restrict__ out) {
-  extern __shared__ __align__(16) double wsm[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  double* R = wsm + wib * C::W * C::W;
   const int r = lane % C::TR;
   const int c = lane / C::TR;
-  for (int e = lane; e < C::W * C::W; e += 32) R[e] = 0.0;
-  __syncwarp();
+  const int64_t gw = (int64_t)blockIdx.x * C::WARPS + wib;
+  if (gw >= nunits) return;
   int cols[C::CPT];
 #pragma unroll
   for (int q = 0; q < C::CPT; ++q) cols[q] = wcol<C>(q, c);
-  const int64_t gw = (int64_t)blockIdx.x * C::WARPS + wib;
-  const int64_t nw = nunits;
-  if (gw >= nunits) return;
+  double Racc[C::RR][C::CPT];
+#pragma unroll
+  for (int m = 0; m < C::RR; ++m)
+#pragma unroll
+    for (int q = 0; q < C::CPT; ++q) Racc[m][q] = 0.0;
 
-  for (int64_t t = gw; t < total_tiles; t += nw) {
+  for (int64_t t = gw; t < total_tiles; t += nunits) {
     double X[C::RPT][C::CPT];
 #pragma unroll
     for (int i = 0; i < C::RPT; ++i) {
@@ -288,56 +297,62 @@ __global__ void __launch_bounds__(C::NT)
 
 #pragma unroll
     for (int k = 0; k < C::W; ++k) {
-      constexpr int dummy = 0;
-      (void)dummy;
       const int qb = k / C::TC;
       const int within = k % C::TC;
       const int ck = (qb & 1) ? C::TC - 1 - within : within;
-      // Pivot column to every lane (same rows r), then the reflector.
+      const int rk = k % C::TR;   // lane row holding accumulator row k
+      const int mk = k / C::TR;
       double v[C::RPT];
-      double s0 = 0.0, s1 = 0.0;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
       for (int i = 0; i < C::RPT; ++i) {
         v[i] = __shfl_sync(0xffffffffu, X[i][qb], r + ck * C::TR);
-        if (i & 1) s1 = fma(v[i], v[i], s1); else s0 = fma(v[i], v[i], s0);
+        if ((i & 3) == 0) s0 = fma(v[i], v[i], s0);
+        else if ((i & 3) == 1) s1 = fma(v[i], v[i], s1);
+        else if ((i & 3) == 2) s2 = fma(v[i], v[i], s2);
+        else s3 = fma(v[i], v[i], s3);
       }
-      const double sig = wgroup_sum<C>(s0 + s1);
-      const double alpha = R[k * C::W + k];
-      if (!(sig > 0.0)) continue;  // warp-uniform: H = I
+      const double sig = wgroup_sum<C>((s0 + s1) + (s2 + s3));
+      const double alpha = __shfl_sync(0xffffffffu, Racc[mk][qb], rk + ck * C::TR);
+      const bool live = sig > 0.0;
       const double nrm = sqrt(fma(alpha, alpha, sig));
-      const double beta = alpha >= 0.0 ? -nrm : nrm;
+      const double beta = live ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
       const double u = alpha - beta;
-      const double inv = 1.0 / (u * beta);
-      const double tau = -u * u * inv;   // (beta - alpha) / beta
-      const double scal = beta * inv;    // 1 / (alpha - beta)
+      const double inv = live ? 1.0 / (u * beta) : 0.0;
+      const double tau = -u * u * inv;   // (beta - alpha) / beta, 0 if !live
+      const double scal = beta * inv;    // 1 / (alpha - beta),    0 if !live
 #pragma unroll
       for (int i = 0; i < C::RPT; ++i) v[i] *= scal;
 #pragma unroll
       for (int q = qb; q < C::CPT; ++q) {
-        const int j = cols[q];
-        const bool act = j > k;
-        const double rkj = R[k * C::W + j];
-        double d0 = 0.0, d1 = 0.0;
+        const bool act = cols[q] > k;
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
         for (int i = 0; i < C::RPT; ++i) {
-          if (i & 1) d1 = fma(v[i], X[i][q], d1); else d0 = fma(v[i], X[i][q], d0);
+          if ((i & 3) == 0) d0 = fma(v[i], X[i][q], d0);
+          else if ((i & 3) == 1) d1 = fma(v[i], X[i][q], d1);
+          else if ((i & 3) == 2) d2 = fma(v[i], X[i][q], d2);
+          else d3 = fma(v[i], X[i][q], d3);
         }
-        const double f = tau * (wgroup_sum<C>(d0 + d1) + rkj);
-        if (act) {
+        double d = (d0 + d1) + (d2 + d3);
+        if (r == rk) d += Racc[mk][q];
+        const double dsum = wgroup_sum<C>(d);  // all lanes shuffle
+        const double f = act ? tau * dsum : 0.0;
 #pragma unroll
-          for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
-        }
-        __syncwarp();
-        if (act && r == 0) R[k * C::W + j] = rkj - f;
+        for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
+        if (r == rk) Racc[mk][q] -= f;
       }
-      __syncwarp();
-      if (lane == 0) R[k * C::W + k] = beta;
-      __syncwarp();
+      if (r == rk && c == ck) Racc[mk][qb] = beta;
     }
   }
-  __syncwarp();
   double* o = out + gw * C::W * C::W;
-  for (int e = lane; e < C::W * C::W; e += 32) o[e] = R[e];
+#pragma unroll
+  for (int m = 0; m < C::RR; ++m)
+#pragma unroll
+    for (int q = 0; q < C::CPT; ++q)
+      if (m * C::TR + r < C::W) o[(m * C::TR + r) * C::W + cols[q]] = Racc[m][q];
+  // Entries of R below the diagonal are never written by the loop (they
+  // stay 0), so the stored factor is upper triangular.
 }
 
 __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
@@ -353,10 +368,24 @@ __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
 
 using C64 = Cfg<64, 32, 8, 16>;
 using C128 = Cfg<128, 32, 8, 8>;
-using W4 = WCfg<4, 8, 8>;
-using W8 = WCfg<8, 8, 8>;
-using W16 = WCfg<16, 4, 16>;
-using W32 = WCfg<32, 2, 16>;
+using W4 = WCfg<4, 1, 8, 2>;
+using W8 = WCfg<8, 2, 8, 2>;
+using W16 = WCfg<16, 2, 8, 2>;
+using W16b = WCfg<16, 2, 16, 1>;
+using W16c = WCfg<16, 4, 8, 2>;
+using W32 = WCfg<32, 2, 8, 2>;
+using W32c = WCfg<32, 4, 8, 2>;
+using C16 = Cfg<16, 8, 16, 16>;
+using C32 = Cfg<32, 16, 16, 8>;
+
+// Kernel variant per width (FG_TSQR_W16 / FG_TSQR_W32 = warp | warpb |
+// warpc | cta) -- a tuning knob; the default is the measured best.
+int variant(int W) {
+  const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32" : "FG_TSQR_X");
+  if (!e) return W == 16 ? 2 : W == 32 ? 3 : 0;  // measured best (tsqr_sweep.py)
+  const std::string v = e;
+  return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : 0;
+}
 
 int bucket(int w) {
   for (int b : {4, 8, 16, 32, 64, 128})
@@ -394,8 +423,16 @@ Plan plan_for(Context& ctx, int W) {
   switch (W) {
     case 4: return plan_warp<W4>(ctx);
     case 8: return plan_warp<W8>(ctx);
-    case 16: return plan_warp<W16>(ctx);
-    case 32: return plan_warp<W32>(ctx);
+    case 16: {
+      const int v = variant(16);
+      return v == 1 ? plan_warp<W16b>(ctx) : v == 2 ? plan_warp<W16c>(ctx)
+             : v == 3 ? plan_cta<C16>(ctx) : plan_warp<W16>(ctx);
+    }
+    case 32: {
+      const int v = variant(32);
+      return v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
+                    : plan_warp<W32>(ctx);
+    }
     case 64: return plan_cta<C64>(ctx);
     default: return plan_cta<C128>(ctx);
   }
@@ -407,8 +444,21 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
   switch (W) {
     case 4: k_tsqr_warp<W4><<<grid, W4::NT, W4::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
     case 8: k_tsqr_warp<W8><<<grid, W8::NT, W8::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 16: k_tsqr_warp<W16><<<grid, W16::NT, W16::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 32: k_tsqr_warp<W32><<<grid, W32::NT, W32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 16: {
+      const int v = variant(16);
+      if (v == 1) k_tsqr_warp<W16b><<<grid, W16b::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 2) k_tsqr_warp<W16c><<<grid, W16c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 3) k_tsqr<C16><<<grid, C16::NT, C16::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else k_tsqr_warp<W16><<<grid, W16::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      break;
+    }
+    case 32: {
+      const int v = variant(32);
+      if (v == 2) k_tsqr_warp<W32c><<<grid, W32c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 3) k_tsqr<C32><<<grid, C32::NT, C32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else k_tsqr_warp<W32><<<grid, W32::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      break;
+    }
     case 64: k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
     default: k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
   }
