@@ -140,10 +140,9 @@ def shard_database(config: str, scale: float, seed: int, rank: int, world: int):
     from paper_2204_00525_b200 import workloads
     db = workloads.make(config, seed=seed + 1000003 * rank, scale=scale)
     if world > 1:
-        span = max(int(r.keys.max()) for r in db.relations if r.keys.size) + 1
         for r in db.relations:
             if r.keys.size:
-                r.keys = r.keys * world + rank if span else r.keys
+                r.keys = r.keys * world + rank
     return db
 
 
@@ -235,13 +234,12 @@ def main():
     n = sum(len(r.data_attrs) for r in db.relations)
     opts = F.PipelineOptions(assume_reduced=True)
 
+    from paper_2204_00525_b200 import distributed as D
+    merge = lambda parts, nn: D.device_merge(parts, nn, device=local)  # noqa: E731
+
     def step():
         res = F.run_pipeline(rels, tree, opts, device=local, fetch_counts=False)
-        R = res.factor.r
-        if world > 1:
-            parts = [torch.empty_like(R) for _ in range(world)]
-            dist.all_gather(parts, R)
-            R = F.tsqr([(p, 0) for p in parts], n, device=local)
+        R = D.gather_and_merge(res.factor.r, merge) if world > 1 else res.factor.r
         return res, R
 
     for _ in range(args.warmup):
@@ -290,10 +288,7 @@ def main():
         hr = F.run_pipeline(host_rels, tree, opts, device=local, fetch_counts=False)
         Rh = hr.factor.r
         if world > 1:
-            Rt = torch.from_numpy(Rh).cuda()
-            parts = [torch.empty_like(Rt) for _ in range(world)]
-            dist.all_gather(parts, Rt)
-            Rh = F.tsqr([(p, 0) for p in parts], n, device=local).cpu().numpy()
+            Rh = D.gather_and_merge(torch.from_numpy(Rh).cuda(), merge).cpu().numpy()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:

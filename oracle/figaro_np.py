@@ -244,6 +244,46 @@ class Layout:
 
 
 # --------------------------------------------------------------------------
+# reduce.hpp
+
+
+class empty_join_error(error):
+    """error.hpp:38-41"""
+
+
+def semi_join(rel: Relation, other: Relation, attrs) -> Relation:
+    """reduce.hpp:20-43: keep rows of rel whose projection occurs in other."""
+    if not attrs:
+        return rel
+    present = {project_key(other.key_tuple(i), other.key_attrs, attrs) for i in range(other.rows)}
+    keep = [i for i in range(rel.rows)
+            if project_key(rel.key_tuple(i), rel.key_attrs, attrs) in present]
+    return Relation(rel.name, rel.key_attrs, rel.data_attrs, rel.keys[keep], rel.data[keep])
+
+
+def semi_join_reduce(rels: List[Relation], tree: JoinTree) -> List[Relation]:
+    """reduce.hpp:47-74: bottom-up then top-down semi-join sweep."""
+    rels = list(rels)
+
+    def nonempty(i):
+        if rels[i].rows == 0:
+            raise empty_join_error("relation %s reduced to empty: the join result is empty"
+                                   % rels[i].name)
+
+    for i in tree.preorder:
+        nonempty(i)
+    for i in reversed(tree.preorder):
+        for c in tree.children[i]:
+            rels[i] = semi_join(rels[i], rels[c], tree.parent_attrs[c])
+            nonempty(i)
+    for i in tree.preorder:
+        for c in tree.children[i]:
+            rels[c] = semi_join(rels[c], rels[i], tree.parent_attrs[c])
+            nonempty(c)
+    return rels
+
+
+# --------------------------------------------------------------------------
 # counts.hpp
 
 
@@ -505,11 +545,14 @@ class PipelineResult:
 
 
 def run_pipeline(rels: List[Relation], root: int, parent: Sequence[int],
-                 canonical: bool = True) -> PipelineResult:
-    """driver.hpp:47-85 with assume_reduced=true and the Householder engine."""
+                 canonical: bool = True, reduce: bool = False) -> PipelineResult:
+    """driver.hpp:47-85 with the Householder engine (assume_reduced unless
+    `reduce`)."""
     if canonical:
         rels = [canonicalize(r) for r in rels]
     tree = build_join_tree(rels, root, parent)
+    if reduce:
+        rels = semi_join_reduce(rels, tree)
     layout = Layout(rels, tree)
     counts = compute_counts(rels, tree)
     r0 = figaro_r0(rels, tree, layout, counts)
