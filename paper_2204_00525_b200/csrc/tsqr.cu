@@ -54,7 +54,7 @@ struct Cfg {
   static constexpr int LDS = W + 1;  // padded staging row (bank spread)
   static_assert(W % TC == 0, "W % TC");
   static_assert(TC % GPW == 0, "TC % GPW");
-  static constexpr size_t smem_doubles = W * W + 2 * B + 2 + B * LDS;
+  static constexpr size_t smem_doubles = W * W + 2 * B + 4 + B * LDS;
   static constexpr size_t smem_bytes = smem_doubles * 8 + B * sizeof(int);
 };
 
@@ -68,6 +68,45 @@ __device__ __forceinline__ double group_sum(double x, unsigned mask) {
 #pragma unroll
   for (int o = C::TR / 2; o; o >>= 1) x += __shfl_xor_sync(mask, x, o);
   return x;
+}
+
+// 1/sqrt(q) and 1/q from the MUFU approximations plus two Newton steps
+// (relative error ~1e-16; the IEEE sqrt+div sequence costs ~184 cycles of
+// latency on B200, this ~60).
+__device__ __forceinline__ double fast_rsqrt(double q) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  const double hq = 0.5 * q;
+  r = r * fma(-hq * r, r, 1.5);
+  r = r * fma(-hq * r, r, 1.5);
+  return r;
+}
+__device__ __forceinline__ double fast_rcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = r * fma(-q, r, 2.0);
+  r = r * fma(-q, r, 2.0);
+  return r;
+}
+
+// Householder reflector of column k with pivot alpha and tail norm^2 sig in
+// the unnormalised form H = I - tau * u u^T, u = [alpha - beta; x]:
+//   beta = -sign(alpha) * ||(alpha, x)||,  tau = 1 / (nrm * (nrm + |alpha|)).
+// tau = 0 when the tail is zero (H = I, beta = alpha).
+struct Reflector {
+  double beta, u0, tau;
+};
+__device__ __forceinline__ Reflector make_reflector(double alpha, double sig) {
+  Reflector h;
+  const double q = fma(alpha, alpha, sig);
+  const bool live = sig > 0.0;
+  const double rs = fast_rsqrt(live ? q : 1.0);
+  const double nrm = q * rs;
+  const double aa = fabs(alpha);
+  h.beta = live ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
+  h.u0 = alpha - h.beta;
+  h.tau = live ? fast_rcp(fma(nrm, aa, q)) : 0.0;
+  return h;
 }
 
 // Issues the cp.async copies of tile `t` (rows t*B .. t*B+B-1 of the
@@ -119,7 +158,8 @@ __global__ void __launch_bounds__(C::NT)
   double* R = sm;                         // W x W
   double* vbuf = R + C::W * C::W;         // 2 x B
   double* taus = vbuf + 2 * C::B;         // 2
-  double* stage = taus + 2;               // B x LDS
+  double* u0s = taus + 2;                 // 2
+  double* stage = u0s + 2;                // B x LDS
   int* rowseg = reinterpret_cast<int*>(stage + C::B * C::LDS);
 
   const int lane = threadIdx.x & 31;
@@ -163,21 +203,21 @@ __global__ void __launch_bounds__(C::NT)
           }
           const double sig = group_sum<C>(s0 + s1, gmask);
           const double alpha = R[k * C::W + k];
-          double tau = 0.0;
-          if (sig > 0.0) {
-            const double nrm = sqrt(fma(alpha, alpha, sig));
-            const double beta = alpha >= 0.0 ? -nrm : nrm;
-            tau = (beta - alpha) / beta;
-            const double scal = 1.0 / (alpha - beta);
+          const Reflector h = make_reflector(alpha, sig);
+          if (h.tau != 0.0) {
 #pragma unroll
-            for (int i = 0; i < C::RPT; ++i) vb[i * C::TR + r] = X[i][qb] * scal;
-            __syncwarp(gmask);
-            if (r == 0) R[k * C::W + k] = beta;
+            for (int i = 0; i < C::RPT; ++i) vb[i * C::TR + r] = X[i][qb];
           }
-          if (r == 0) taus[k & 1] = tau;
+          __syncwarp(gmask);
+          if (r == 0) {
+            R[k * C::W + k] = h.beta;
+            taus[k & 1] = h.tau;
+            u0s[k & 1] = h.u0;
+          }
         }
         __syncthreads();
         const double tau = taus[k & 1];
+        const double u0 = u0s[k & 1];
         if (tau == 0.0) continue;
         double v[C::RPT];
 #pragma unroll
@@ -194,11 +234,11 @@ __global__ void __launch_bounds__(C::NT)
             if (i + 1 < C::RPT) d1 = fma(v[i + 1], X[i + 1][q], d1);
           }
           const double d = group_sum<C>(d0 + d1, gmask);
-          const double f = tau * (d + rkj);
+          const double f = tau * fma(u0, rkj, d);
 #pragma unroll
           for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
           __syncwarp(gmask);
-          if (r == 0) R[k * C::W + j] = rkj - f;
+          if (r == 0) R[k * C::W + j] = fma(-f, u0, rkj);
         }
       }
     }
@@ -314,15 +354,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
       const double sig = wgroup_sum<C>((s0 + s1) + (s2 + s3));
       const double alpha = __shfl_sync(0xffffffffu, Racc[mk][qb], rk + ck * C::TR);
-      const bool live = sig > 0.0;
-      const double nrm = sqrt(fma(alpha, alpha, sig));
-      const double beta = live ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
-      const double u = alpha - beta;
-      const double inv = live ? 1.0 / (u * beta) : 0.0;
-      const double tau = -u * u * inv;   // (beta - alpha) / beta, 0 if !live
-      const double scal = beta * inv;    // 1 / (alpha - beta),    0 if !live
-#pragma unroll
-      for (int i = 0; i < C::RPT; ++i) v[i] *= scal;
+      const Reflector h = make_reflector(alpha, sig);
 #pragma unroll
       for (int q = qb; q < C::CPT; ++q) {
         const bool act = cols[q] > k;
@@ -335,14 +367,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
           else d3 = fma(v[i], X[i][q], d3);
         }
         double d = (d0 + d1) + (d2 + d3);
-        if (r == rk) d += Racc[mk][q];
+        if (r == rk) d = fma(h.u0, Racc[mk][q], d);
         const double dsum = wgroup_sum<C>(d);  // all lanes shuffle
-        const double f = act ? tau * dsum : 0.0;
+        const double f = act ? h.tau * dsum : 0.0;
 #pragma unroll
         for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
-        if (r == rk) Racc[mk][q] -= f;
+        if (r == rk) Racc[mk][q] = fma(-f, h.u0, Racc[mk][q]);
       }
-      if (r == rk && c == ck) Racc[mk][qb] = beta;
+      if (r == rk && c == ck) Racc[mk][qb] = h.beta;
     }
   }
   double* o = out + gw * C::W * C::W;
@@ -371,7 +403,7 @@ using C128 = Cfg<128, 32, 8, 8>;
 using W4 = WCfg<4, 1, 8, 2>;
 using W8 = WCfg<8, 2, 8, 2>;
 using W16 = WCfg<16, 2, 8, 2>;
-using W16b = WCfg<16, 2, 16, 1>;
+using W16b = WCfg<16, 2, 16, 2>;
 using W16c = WCfg<16, 4, 8, 2>;
 using W32 = WCfg<32, 2, 8, 2>;
 using W32c = WCfg<32, 4, 8, 2>;

@@ -1,0 +1,96 @@
+// GPU parity through the C++ facade (include/figaro_gpu.hpp) on the
+// reference's own types: random_acyclic_database (testbench.hpp:164) and the
+// four-relation fixture shape, reference run_pipeline (driver.hpp:47) vs
+// figaro::gpu::run_pipeline.  Test infrastructure: built by oracle/Makefile
+// against /root/reference headers; run by tests/test_gpu_parity.py.
+#include <cmath>
+#include <cstdio>
+
+#include "figaro/driver.hpp"
+#include "figaro/testbench.hpp"
+#include "figaro_gpu.hpp"
+
+namespace {
+
+struct RefErrors {
+  [[noreturn]] static void raise(fg_status st, const std::string& m) {
+    switch (st) {
+      case FG_E_INTEGRITY: throw figaro::integrity_error(m);
+      case FG_E_SIZE: throw figaro::size_error(m);
+      case FG_E_TREE: throw figaro::tree_error(m);
+      case FG_E_SCHEMA: throw figaro::schema_error(m);
+      case FG_E_EMPTY_JOIN: throw figaro::empty_join_error(m);
+      default: throw figaro::error(m);
+    }
+  }
+};
+
+double rel_dist(const std::vector<double>& a, const figaro::Matrix& b, bool gram) {
+  const std::size_t n = b.rows();
+  double diff = 0, ref = 0;
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = 0; j < n; ++j) {
+      double x = 0, y = 0;
+      if (gram) {
+        for (std::size_t k = 0; k < n; ++k) {
+          x += a[k * n + i] * a[k * n + j];
+          y += b(k, i) * b(k, j);
+        }
+      } else {
+        x = a[i * n + j];
+        y = b(i, j);
+      }
+      diff += (x - y) * (x - y);
+      ref += y * y;
+    }
+  return ref == 0 ? std::sqrt(diff) : std::sqrt(diff / ref);
+}
+
+}  // namespace
+
+int main() {
+  figaro::gpu::Device dev(0);
+  int bad = 0;
+  double worst = 0;
+  for (std::uint64_t seed = 1; seed <= 40; ++seed) {
+    figaro::bench::RandomDbSpec spec;
+    spec.max_rows = 300;
+    spec.key_domain = 6;
+    auto db = figaro::bench::random_acyclic_database(spec, seed * 31);
+    figaro::PipelineOptions opts;
+    opts.assume_reduced = true;
+    auto ref = figaro::run_pipeline(db.relations, db.tree, opts);
+    auto got = figaro::gpu::run_pipeline<figaro::Relation, figaro::JoinTree, RefErrors>(
+        dev, db.relations, db.tree, true);
+    bool full = ref.factor.zero_diagonal_rows.empty();
+    for (std::size_t i = 0; i < ref.factor.r.rows() && full; ++i)
+      full = std::abs(ref.factor.r(i, i)) > 1e-8 * std::abs(ref.factor.r(0, 0));
+    const double d = rel_dist(got.r, ref.factor.r, !full);
+    worst = std::max(worst, d);
+    if (d > 1e-10 || got.r0_rows != ref.r0_rows || got.input_rows != ref.input_rows) {
+      ++bad;
+      std::printf("seed %llu: dist %.3e r0 %zu/%zu\n", (unsigned long long)seed, d,
+                  got.r0_rows, ref.r0_rows);
+    }
+  }
+  // Unreduced input: integrity_error through the facade, like the reference.
+  figaro::bench::RandomDbSpec spec;
+  auto db = figaro::bench::random_acyclic_database(spec, 5);
+  db.relations[0].keys.push_back(db.relations[0].keys[0]);
+  for (auto& v : db.relations[0].keys.back())
+    if (std::holds_alternative<std::int64_t>(v)) v = std::int64_t{987654};
+  db.relations[0].data.resize(db.relations[0].keys.size(), db.relations[0].data.cols());
+  bool threw = false;
+  try {
+    figaro::gpu::run_pipeline<figaro::Relation, figaro::JoinTree, RefErrors>(
+        dev, db.relations, db.tree, true);
+  } catch (const figaro::integrity_error&) {
+    threw = true;
+  }
+  if (db.relations.size() > 1 && !threw) {
+    ++bad;
+    std::printf("unreduced input did not raise integrity_error\n");
+  }
+  std::printf("%s facade parity: 40 databases, worst %.3e\n", bad ? "FAIL" : "PASS", worst);
+  return bad ? 1 : 0;
+}
