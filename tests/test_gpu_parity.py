@@ -229,3 +229,14 @@ def test_full_size_c2_gram_property():
     ata[:16, 16:] = cross
     ata[16:, :16] = cross.T
     assert fo.rel_frobenius_distance(R.T @ R, ata) <= 1e-12
+
+
+def test_cpp_facade_on_reference_types():
+    """include/figaro_gpu.hpp bound to the reference's own Relation/JoinTree
+    (tests/cpp/facade_parity.cpp, built by oracle/Makefile)."""
+    exe = os.path.join(os.path.dirname(REF_BIN), "facade_parity")
+    if not os.path.exists(exe):
+        pytest.skip("facade_parity not built")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "PASS" in out.stdout
