@@ -55,8 +55,9 @@ __global__ void k_key_minmax(const int64_t* __restrict__ keys, int64_t rows,
   }
 }
 
+template <class KeyT>
 __global__ void k_pack_keys(const int64_t* __restrict__ keys, int64_t rows,
-                            int n_key, PackSpec spec, uint64_t* __restrict__ out,
+                            int n_key, PackSpec spec, KeyT* __restrict__ out,
                             int* __restrict__ iota) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -67,7 +68,7 @@ __global__ void k_pack_keys(const int64_t* __restrict__ keys, int64_t rows,
       const uint64_t enc = (uint64_t)v - (uint64_t)spec.min[f];
       if (spec.bits[f]) k |= enc << spec.shift[f];
     }
-    out[i] = k;
+    out[i] = static_cast<KeyT>(k);
     if (iota) iota[i] = static_cast<int>(i);
   }
 }
@@ -156,6 +157,20 @@ __global__ void k_seg_sizes(const int* __restrict__ begins, int64_t G,
 
 __global__ void k_set_last(int* begins, int64_t G, int n) { begins[G] = n; }
 
+__global__ void k_narrow(const uint64_t* __restrict__ in, int64_t n,
+                         uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = static_cast<uint32_t>(in[i]);
+}
+
+__global__ void k_widen(const uint32_t* __restrict__ in, int64_t n,
+                        uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
 }  // namespace
 
 void launch_key_minmax(Context& ctx, const int64_t* keys, int64_t rows,
@@ -169,11 +184,11 @@ void launch_key_minmax(Context& ctx, const int64_t* keys, int64_t rows,
   FG_KERNEL_CHECK();
 }
 
+template <class KeyT>
 void launch_pack_keys(Context& ctx, const int64_t* keys, int64_t rows,
-                      int n_key, const PackSpec& spec, uint64_t* out,
-                      int* iota) {
+                      int n_key, const PackSpec& spec, KeyT* out, int* iota) {
   if (rows == 0) return;
-  k_pack_keys<<<grid_for(ctx, rows), kThreads, 0, ctx.stream>>>(
+  k_pack_keys<KeyT><<<grid_for(ctx, rows), kThreads, 0, ctx.stream>>>(
       keys, rows, n_key, spec, out, iota);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
@@ -220,11 +235,12 @@ void launch_seg_sizes(Context& ctx, const int* begins, int64_t G,
   FG_KERNEL_CHECK();
 }
 
-void sort_pairs(Context& ctx, const uint64_t* keys_in, uint64_t* keys_out,
+template <class KeyT>
+void sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out,
                 const int* vals_in, int* vals_out, int64_t n, int bits) {
   if (n == 0) return;
   if (bits == 0) {
-    FG_CUDA(cudaMemcpyAsync(keys_out, keys_in, n * sizeof(uint64_t),
+    FG_CUDA(cudaMemcpyAsync(keys_out, keys_in, n * sizeof(KeyT),
                             cudaMemcpyDeviceToDevice, ctx.stream));
     FG_CUDA(cudaMemcpyAsync(vals_out, vals_in, n * sizeof(int),
                             cudaMemcpyDeviceToDevice, ctx.stream));
@@ -241,8 +257,9 @@ void sort_pairs(Context& ctx, const uint64_t* keys_in, uint64_t* keys_out,
   ctx.launches += (bits + 7) / 8 + 1;
 }
 
-void run_length(Context& ctx, const uint64_t* sorted, int64_t n,
-                uint64_t* uniq, int* counts, int64_t* num_runs_dev) {
+template <class KeyT>
+void run_length(Context& ctx, const KeyT* sorted, int64_t n,
+                KeyT* uniq, int* counts, int64_t* num_runs_dev) {
   size_t temp = 0;
   FG_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, temp, sorted, uniq,
                                              counts, num_runs_dev, n,
@@ -287,15 +304,16 @@ void launch_run_ids(Context& ctx, const uint64_t* sorted, const int* perm,
   FG_KERNEL_CHECK();
 }
 
-void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
-                  const int* perm_in, GroupOut& out, bool keep_sorted) {
+template <class KeyT>
+void group_sorted_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
+                    const int* perm_in, GroupOut& out, bool keep_sorted) {
   out.perm.alloc(n, ctx.stream);
-  DevArray<uint64_t> sorted(n, ctx.stream);
-  sort_pairs(ctx, keys, sorted.get(), perm_in, out.perm.get(), n, bits);
-  DevArray<uint64_t> uniq(n, ctx.stream);
+  DevArray<KeyT> sorted(n, ctx.stream);
+  sort_pairs<KeyT>(ctx, keys, sorted.get(), perm_in, out.perm.get(), n, bits);
+  DevArray<KeyT> uniq(n, ctx.stream);
   DevArray<int> counts(n + 1, ctx.stream);
   DevArray<int64_t> nr(1, ctx.stream);
-  run_length(ctx, sorted.get(), n, uniq.get(), counts.get(), nr.get());
+  run_length<KeyT>(ctx, sorted.get(), n, uniq.get(), counts.get(), nr.get());
   int64_t G = 0;
   FG_CUDA(cudaMemcpyAsync(&G, nr.get(), sizeof G, cudaMemcpyDeviceToHost,
                           ctx.stream));
@@ -306,10 +324,43 @@ void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
   k_set_last<<<1, 1, 0, ctx.stream>>>(out.begins.get(), G, static_cast<int>(n));
   FG_LAUNCHED(ctx);
   out.uniq.alloc(G, ctx.stream);
-  if (G)
-    FG_CUDA(cudaMemcpyAsync(out.uniq.get(), uniq.get(), G * sizeof(uint64_t),
-                            cudaMemcpyDeviceToDevice, ctx.stream));
-  if (keep_sorted) out.sorted = std::move(sorted);
+  if (G) {
+    if constexpr (sizeof(KeyT) == 8) {
+      FG_CUDA(cudaMemcpyAsync(out.uniq.get(), uniq.get(), G * sizeof(uint64_t),
+                              cudaMemcpyDeviceToDevice, ctx.stream));
+    } else {
+      k_widen<<<grid_for(ctx, G), kThreads, 0, ctx.stream>>>(
+          reinterpret_cast<const uint32_t*>(uniq.get()), G, out.uniq.get());
+      FG_LAUNCHED(ctx);
+      FG_KERNEL_CHECK();
+    }
+  }
+  if (keep_sorted) {
+    if constexpr (sizeof(KeyT) == 8) {
+      out.sorted = std::move(sorted);
+    } else {
+      out.sorted.alloc(n, ctx.stream);
+      k_widen<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(
+          reinterpret_cast<const uint32_t*>(sorted.get()), n, out.sorted.get());
+      FG_LAUNCHED(ctx);
+      FG_KERNEL_CHECK();
+    }
+  }
 }
+
+void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
+                  const int* perm_in, GroupOut& out, bool keep_sorted) {
+  group_sorted_t<uint64_t>(ctx, keys, n, bits, perm_in, out, keep_sorted);
+}
+
+void group_sorted32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
+                    const int* perm_in, GroupOut& out, bool keep_sorted) {
+  group_sorted_t<uint32_t>(ctx, keys, n, bits, perm_in, out, keep_sorted);
+}
+
+template void launch_pack_keys<uint64_t>(Context&, const int64_t*, int64_t, int,
+                                         const PackSpec&, uint64_t*, int*);
+template void launch_pack_keys<uint32_t>(Context&, const int64_t*, int64_t, int,
+                                         const PackSpec&, uint32_t*, int*);
 
 }  // namespace fg

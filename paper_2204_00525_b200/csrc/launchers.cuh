@@ -25,9 +25,9 @@ void launch_key_minmax(Context& ctx, const int64_t* keys, int64_t rows,
                        long long* mins, long long* maxs);
 // Packs int64 key tuples into u64 keys (declaration order, MSB first) and
 // writes the identity permutation.
+template <class KeyT>
 void launch_pack_keys(Context& ctx, const int64_t* keys, int64_t rows,
-                      int n_key, const PackSpec& spec, uint64_t* out,
-                      int* iota);
+                      int n_key, const PackSpec& spec, KeyT* out, int* iota);
 // Re-packs already packed keys into another field layout (projection).
 void launch_project(Context& ctx, const uint64_t* in, int64_t n,
                     const PackSpec& from_to, uint64_t* out);
@@ -42,14 +42,19 @@ struct GroupOut {
 };
 void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
                   const int* perm_in, GroupOut& out, bool keep_sorted = false);
+// Same with 32-bit packed keys (own keys of <= 32 significant bits).
+void group_sorted32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
+                    const int* perm_in, GroupOut& out, bool keep_sorted = false);
 // Without syncing: sort only (keys_out/perm_out) -- used when the caller
 // batches syncs itself.
-void sort_pairs(Context& ctx, const uint64_t* keys_in, uint64_t* keys_out,
+template <class KeyT>
+void sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out,
                 const int* vals_in, int* vals_out, int64_t n, int bits);
 // Run-length encode a sorted key array. Writes uniq, counts and *num_runs
 // (device); no sync.
-void run_length(Context& ctx, const uint64_t* sorted, int64_t n,
-                uint64_t* uniq, int* counts, int64_t* num_runs_dev);
+template <class KeyT>
+void run_length(Context& ctx, const KeyT* sorted, int64_t n,
+                KeyT* uniq, int* counts, int64_t* num_runs_dev);
 void exclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
 void inclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
 // pidx[perm[s]] = run id of sorted position s.

@@ -553,23 +553,32 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
                                      n.key_attr.begin());
                       },
                       &n.own_bits, "relation " + n.name);
-    DevArray<uint64_t> pk(n.rows, st);
-    DevArray<int> iota;
-    if (n.rows) {
-      if (n.has_sel) {
-        k_pack_sel<<<grid1d(ctx, n.rows), 256, 0, st>>>(n.keys, n.n_key,
-                                                        n.sel.get(), n.rows,
-                                                        n.own, pk.get());
-        FG_LAUNCHED(ctx);
-        FG_KERNEL_CHECK();
-      } else {
-        iota.alloc(n.rows, st);
-        launch_pack_keys(ctx, n.keys, n.rows, n.n_key, n.own, pk.get(),
-                         iota.get());
+    if (n.own_bits <= 32 && !n.has_sel) {
+      // Narrow packed keys: 8 instead of 12 bytes per element per radix pass.
+      DevArray<uint32_t> pk(n.rows, st);
+      DevArray<int> iota(n.rows, st);
+      launch_pack_keys<uint32_t>(ctx, n.keys, n.rows, n.n_key, n.own, pk.get(),
+                                 iota.get());
+      group_sorted32(ctx, pk.get(), n.rows, n.own_bits, iota.get(), n.grp);
+    } else {
+      DevArray<uint64_t> pk(n.rows, st);
+      DevArray<int> iota;
+      if (n.rows) {
+        if (n.has_sel) {
+          k_pack_sel<<<grid1d(ctx, n.rows), 256, 0, st>>>(n.keys, n.n_key,
+                                                          n.sel.get(), n.rows,
+                                                          n.own, pk.get());
+          FG_LAUNCHED(ctx);
+          FG_KERNEL_CHECK();
+        } else {
+          iota.alloc(n.rows, st);
+          launch_pack_keys<uint64_t>(ctx, n.keys, n.rows, n.n_key, n.own,
+                                     pk.get(), iota.get());
+        }
       }
+      group_sorted(ctx, pk.get(), n.rows, n.own_bits,
+                   n.has_sel ? n.sel.get() : iota.get(), n.grp);
     }
-    group_sorted(ctx, pk.get(), n.rows, n.own_bits,
-                 n.has_sel ? n.sel.get() : iota.get(), n.grp);
     n.sizes.alloc(n.grp.G, st);
     launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
   }
