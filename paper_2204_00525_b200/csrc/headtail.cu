@@ -84,7 +84,17 @@ struct WarpSmem {
   double wt[kMaxRB];      // generalized weights
   int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
   const double* rowptr[kMaxRB];
+  int win[kMaxRB + 2];    // begins[g .. g + nb + 1] of the current batch
 };
+
+__device__ __forceinline__ double fast_rsqrt_d(double q) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  const double hq = 0.5 * q;
+  r = r * fma(-hq * r, r, 1.5);
+  r = r * fma(-hq * r, r, 1.5);
+  return r;
+}
 
 // Lane geometry: the warp is split into G row-groups of L lanes; lane cl of
 // a group owns column packets cl + L*s (s < SLOTS) of VEC doubles each.
@@ -175,8 +185,12 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
   for (int64_t pb = p0; pb < p1; pb += a.rb) {
     const int nb = (int)(p1 - pb < (int64_t)a.rb ? p1 - pb : (int64_t)a.rb);
     if (w > 0) stage_rows<SLOTS, VEC>(a, geo, sm, pb, nb, lane);
-    // Row metadata and coefficients, one row per lane.
+    // Row metadata and coefficients, one row per lane.  The group bounds
+    // of the batch come from one coalesced load of begins[g .. g+nb+1].
     const int64_t g_hi = (g + nb + 1 < a.n_seg) ? g + nb + 1 : a.n_seg;
+    const int nwin = (int)(g_hi - g) + 1;
+    for (int t = lane; t < nwin; t += 32) sm.win[t] = a.begins[g + t];
+    __syncwarp();
     for (int base = 0; base < nb; base += 32) {
       const int rr = base + lane;
       const bool live = rr < nb;
@@ -185,29 +199,35 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
       double v = 1.0;
       int fl = 0;
       if (live) {
-        const int64_t p = pb + rr;
-        sg = seg_of(a.begins, p, g, g_hi);
-        const int64_t b0 = a.begins[sg];
-        const int64_t b1 = a.begins[sg + 1];
+        const int p = (int)(pb + rr);
+        int lo = 0, hi = nwin - 1;  // last window slot with win[slot] <= p
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (sm.win[mid] <= p) lo = mid; else hi = mid;
+        }
+        sg = g + lo;
+        const int b0 = sm.win[lo];
+        const int b1 = sm.win[lo + 1];
         jj = p - b0;
         m = b1 - b0;
         fl = (jj == 0 ? 1 : 0) | (p == b1 - 1 ? 2 : 0);
         if (weighted) v = a.weights[src_row(a, p)];
       }
       double ts = 1.0;
-      if (live && a.tail_count) ts = sqrt((double)a.tail_count[sg]);
+      if (live && a.tail_count) ts = sqrt((double)a.tail_count[sg]);  // exact for squares
       double al = 0.0, be = 0.0, hc = 0.0, sc = 0.0;
       if (!weighted) {
         if (live && jj >= 1) {
-          const double sj = sqrt((double)jj);
-          const double sj1 = sqrt((double)(jj + 1));
-          al = sj / sj1 * ts;
-          be = ts / (sj * sj1);
+          // sqrt(j)/sqrt(j+1) and 1/(sqrt(j) sqrt(j+1)) from one rsqrt.
+          const double q = (double)jj * (double)(jj + 1);
+          const double rq = fast_rsqrt_d(q);
+          al = (double)jj * rq * ts;
+          be = ts * rq;
         }
         if (live && (fl & 2)) {
-          const double sm_ = sqrt((double)m);
-          hc = 1.0 / sm_;
-          sc = sm_;
+          const double rm = fast_rsqrt_d((double)m);
+          hc = rm;
+          sc = (double)m * rm;
         }
       } else {
         // Segmented inclusive scan of v^2 over the 32 rows of this chunk.
@@ -447,33 +467,39 @@ __global__ void k_carry_chain(int64_t n_units, int V, const int* __restrict__ co
   }
 }
 
-// K4: joins child summaries into the node's summary rows.
-__global__ void k_join(JoinArgs a) {
+// K4: joins child summaries into the node's summary rows
+// (figaro.hpp:196-230).  One warp per row; lanes over the row's columns.
+// Child scales are re-read per use instead of kept in a dynamically indexed
+// array (which would live in local memory).
+__global__ void __launch_bounds__(256) k_join(const __grid_constant__ JoinArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t k = warp; k < a.G; k += nw) {
-    double cs[kMaxChildren];
-    int idx[kMaxChildren];
-    double all = 1.0;
-    for (int c = 0; c < a.n_children; ++c) {
-      idx[c] = a.lidx[c][k];
-      cs[c] = idx[c] >= 0 ? a.child_scale[c][idx[c]] : 0.0;
-      all *= cs[c];
+    // Lane c (< n_children) loads child c's row index and scale.
+    int my_idx = -1;
+    double my_s = 1.0;
+    if (lane < a.n_children) {
+      my_idx = a.lidx[lane][k];
+      my_s = my_idx >= 0 ? a.child_scale[lane][my_idx] : 0.0;
     }
+    double all = 1.0;
+    for (int c = 0; c < a.n_children; ++c) all *= __shfl_sync(0xffffffffu, my_s, c);
     double* dst = a.S + k * a.width;
     const double sk = a.scale[k];
     for (int c = 0; c < a.n_children; ++c) {
-      if (idx[c] < 0) continue;
+      const int idx = __shfl_sync(0xffffffffu, my_idx, c);
       double factor = sk;
-      for (int d = 0; d < a.n_children; ++d)
-        if (d != c) factor *= cs[d];
-      const double* src = a.child_S[c] + (int64_t)idx[c] * a.child_w[c];
+      for (int d = 0; d < a.n_children; ++d) {
+        const double sd = __shfl_sync(0xffffffffu, my_s, d);
+        if (d != c) factor *= sd;
+      }
+      if (idx < 0) continue;
+      const double* src = a.child_S[c] + (int64_t)idx * a.child_w[c];
       for (int j = lane; j < a.child_w[c]; j += 32)
         dst[a.child_off[c] + j] = src[j] * factor;
     }
     for (int j = lane; j < a.own_w; j += 32) dst[j] *= all;
-    __syncwarp();
     if (lane == 0) a.scale[k] = sk * all;
   }
 }

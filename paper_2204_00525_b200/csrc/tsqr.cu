@@ -54,7 +54,7 @@ struct Cfg {
   static constexpr int LDS = W + 1;  // padded staging row (bank spread)
   static_assert(W % TC == 0, "W % TC");
   static_assert(TC % GPW == 0, "TC % GPW");
-  static constexpr size_t smem_doubles = W * W + 2 * B + 4 + B * LDS;
+  static constexpr size_t smem_doubles = W * W + 2 * B + 6 + B * LDS;
   static constexpr size_t smem_bytes = smem_doubles * 8 + B * sizeof(int);
 };
 
@@ -91,21 +91,35 @@ __device__ __forceinline__ double fast_rcp(double q) {
 
 // Householder reflector of column k with pivot alpha and tail norm^2 sig in
 // the unnormalised form H = I - tau * u u^T, u = [alpha - beta; x]:
-//   beta = -sign(alpha) * ||(alpha, x)||,  tau = 1 / (nrm * (nrm + |alpha|)).
-// tau = 0 when the tail is zero (H = I, beta = alpha).
+//   beta = -sign(alpha) * nrm,  nrm = ||(alpha, x)||,
+//   tau  = 1 / (nrm * (nrm + |alpha|)) = t1 * t2,
+// kept as the two bounded factors t1 = 1/nrm and t2 = 1/(nrm + |alpha|)
+// (tau itself overflows for numerically zero columns, nrm < 1e-154).
+// Callers form g = (d * t1) * t2.  t1 = t2 = 0 when the tail is zero
+// (H = I, beta = alpha).
 struct Reflector {
-  double beta, u0, tau;
+  double beta, u0, t1, t2;
 };
 __device__ __forceinline__ Reflector make_reflector(double alpha, double sig) {
   Reflector h;
   const double q = fma(alpha, alpha, sig);
   const bool live = sig > 0.0;
-  const double rs = fast_rsqrt(live ? q : 1.0);
-  const double nrm = q * rs;
   const double aa = fabs(alpha);
+  double nrm, t1, t2;
+  if (q > 1e-250 && q < 1e250) {
+    // The .ftz approximations flush subnormals: only inside a safe range.
+    t1 = fast_rsqrt(q);
+    nrm = q * t1;
+    t2 = fast_rcp(nrm + aa);
+  } else {
+    nrm = sqrt(q);
+    t1 = 1.0 / nrm;
+    t2 = 1.0 / (nrm + aa);
+  }
   h.beta = live ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
   h.u0 = alpha - h.beta;
-  h.tau = live ? fast_rcp(fma(nrm, aa, q)) : 0.0;
+  h.t1 = live ? t1 : 0.0;
+  h.t2 = live ? t2 : 0.0;
   return h;
 }
 
@@ -157,8 +171,8 @@ __global__ void __launch_bounds__(C::NT)
   extern __shared__ __align__(16) double sm[];
   double* R = sm;                         // W x W
   double* vbuf = R + C::W * C::W;         // 2 x B
-  double* taus = vbuf + 2 * C::B;         // 2
-  double* u0s = taus + 2;                 // 2
+  double* taus = vbuf + 2 * C::B;         // 2 x {t1, t2}
+  double* u0s = taus + 4;                 // 2
   double* stage = u0s + 2;                // B x LDS
   int* rowseg = reinterpret_cast<int*>(stage + C::B * C::LDS);
 
@@ -204,21 +218,23 @@ __global__ void __launch_bounds__(C::NT)
           const double sig = group_sum<C>(s0 + s1, gmask);
           const double alpha = R[k * C::W + k];
           const Reflector h = make_reflector(alpha, sig);
-          if (h.tau != 0.0) {
+          if (h.t1 != 0.0) {
 #pragma unroll
             for (int i = 0; i < C::RPT; ++i) vb[i * C::TR + r] = X[i][qb];
           }
           __syncwarp(gmask);
           if (r == 0) {
             R[k * C::W + k] = h.beta;
-            taus[k & 1] = h.tau;
+            taus[2 * (k & 1)] = h.t1;
+            taus[2 * (k & 1) + 1] = h.t2;
             u0s[k & 1] = h.u0;
           }
         }
         __syncthreads();
-        const double tau = taus[k & 1];
+        const double t1 = taus[2 * (k & 1)];
+        const double t2 = taus[2 * (k & 1) + 1];
         const double u0 = u0s[k & 1];
-        if (tau == 0.0) continue;
+        if (t1 == 0.0) continue;
         double v[C::RPT];
 #pragma unroll
         for (int i = 0; i < C::RPT; ++i) v[i] = vb[i * C::TR + r];
@@ -234,7 +250,7 @@ __global__ void __launch_bounds__(C::NT)
             if (i + 1 < C::RPT) d1 = fma(v[i + 1], X[i + 1][q], d1);
           }
           const double d = group_sum<C>(d0 + d1, gmask);
-          const double f = tau * fma(u0, rkj, d);
+          const double f = (fma(u0, rkj, d) * t1) * t2;
 #pragma unroll
           for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
           __syncwarp(gmask);
@@ -369,7 +385,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         double d = (d0 + d1) + (d2 + d3);
         if (r == rk) d = fma(h.u0, Racc[mk][q], d);
         const double dsum = wgroup_sum<C>(d);  // all lanes shuffle
-        const double f = act ? h.tau * dsum : 0.0;
+        const double f = act ? (dsum * h.t1) * h.t2 : 0.0;
 #pragma unroll
         for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
         if (r == rk) Racc[mk][q] = fma(-f, h.u0, Racc[mk][q]);
