@@ -25,7 +25,10 @@
 // All results are run-to-run deterministic.
 #include <cuda_pipeline.h>
 
+#include <type_traits>
+
 #include "launchers.cuh"
+#include "tsqr_warp.cuh"
 
 namespace fg {
 
@@ -77,15 +80,19 @@ __device__ __forceinline__ int64_t seg_of(const int* __restrict__ begins,
   return lo;
 }
 
-struct WarpSmem {
-  double buf[kSmemDoubles];
+struct NoFuse {};
+
+template <int CAP>
+struct WarpSmemT {
+  double buf[CAP];
   double2 coef[kMaxRB];   // {alpha, beta}: tail = a*alpha - S*beta
   double hco[kMaxRB];     // head coefficient at a group's last row
   double wt[kMaxRB];      // generalized weights
   int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
   const double* rowptr[kMaxRB];
-  int win[kMaxRB + 2];    // begins[g .. g + nb + 1] of the current batch
 };
+using WarpSmem = WarpSmemT<kSmemDoubles>;
+constexpr int kFusedDoubles = 1024;  // one TSQR tile of tails (B x w)
 
 __device__ __forceinline__ double fast_rsqrt_d(double q) {
   double r;
@@ -108,9 +115,9 @@ __device__ __forceinline__ void cp_async(double* dst, const double* src) {
 }
 
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
-template <int SLOTS, int VEC>
+template <int SLOTS, int VEC, class SM>
 __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
-                                           WarpSmem& sm, int64_t p, int nb,
+                                           SM& sm, int64_t p, int nb,
                                            int lane) {
   for (int rr = lane; rr < nb; rr += 32)
     sm.rowptr[rr] = a.data + src_row(a, p + rr) * a.ld;
@@ -128,9 +135,13 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
   __pipeline_commit();
 }
 
-template <int SLOTS, int VEC>
-__device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
-                             int64_t u, int lane) {
+// F = NoFuse: tails are written to a.tails.  F = WCfg<...>: each batch of
+// tails is written in place into the staged rows (group starts become zero
+// rows) and absorbed into the warp's TSQR accumulator Racc.
+template <int SLOTS, int VEC, class F, class SM, class RA>
+__device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
+                             int64_t u, int lane, RA& Racc) {
+  constexpr bool FUSED = !std::is_same<F, NoFuse>::value;
   const int w = a.w;
   const bool weighted = a.weights != nullptr;
   const int64_t p0 = u * kUnit;
@@ -185,12 +196,8 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
   for (int64_t pb = p0; pb < p1; pb += a.rb) {
     const int nb = (int)(p1 - pb < (int64_t)a.rb ? p1 - pb : (int64_t)a.rb);
     if (w > 0) stage_rows<SLOTS, VEC>(a, geo, sm, pb, nb, lane);
-    // Row metadata and coefficients, one row per lane.  The group bounds
-    // of the batch come from one coalesced load of begins[g .. g+nb+1].
+    // Row metadata and coefficients, one row per lane.
     const int64_t g_hi = (g + nb + 1 < a.n_seg) ? g + nb + 1 : a.n_seg;
-    const int nwin = (int)(g_hi - g) + 1;
-    for (int t = lane; t < nwin; t += 32) sm.win[t] = a.begins[g + t];
-    __syncwarp();
     for (int base = 0; base < nb; base += 32) {
       const int rr = base + lane;
       const bool live = rr < nb;
@@ -199,15 +206,10 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
       double v = 1.0;
       int fl = 0;
       if (live) {
-        const int p = (int)(pb + rr);
-        int lo = 0, hi = nwin - 1;  // last window slot with win[slot] <= p
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (sm.win[mid] <= p) lo = mid; else hi = mid;
-        }
-        sg = g + lo;
-        const int b0 = sm.win[lo];
-        const int b1 = sm.win[lo + 1];
+        const int64_t p = pb + rr;
+        sg = seg_of(a.begins, p, g, g_hi);
+        const int64_t b0 = a.begins[sg];
+        const int64_t b1 = a.begins[sg + 1];
         jj = p - b0;
         m = b1 - b0;
         fl = (jj == 0 ? 1 : 0) | (p == b1 - 1 ? 2 : 0);
@@ -370,7 +372,14 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
             o[e] = x[e] * cf.x - run[s][e] * cf.y;
             run[s][e] = weighted ? fma(vw, x[e], run[s][e]) : run[s][e] + x[e];
           }
-          if (trow) {
+          if constexpr (FUSED) {
+            double* slot = const_cast<double*>(row) + VEC * pk;
+            if (VEC == 2)
+              *reinterpret_cast<double2*>(slot) = (sf.y & 1) ? make_double2(0.0, 0.0)
+                                                             : make_double2(o[0], o[VEC - 1]);
+            else
+              slot[0] = (sf.y & 1) ? 0.0 : o[0];
+          } else if (trow) {
             if (VEC == 2)
               *reinterpret_cast<double2*>(trow + 2 * pk) = make_double2(o[0], o[VEC - 1]);
             else
@@ -381,6 +390,26 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, WarpSmem& sm,
             for (int e = 0; e < VEC; ++e) hrow[VEC * pk + e] = run[s][e] * hc;
           }
         }
+      }
+    }
+    if constexpr (FUSED) {
+      if (w > 0) {
+        // The batch (nb <= B rows of tails, zero rows at group starts) is
+        // one TSQR tile for this warp's accumulator.
+        __syncwarp();
+        const int r = lane % F::TR, c = lane / F::TR;
+        int cols[F::CPT];
+        double X[F::RPT][F::CPT];
+#pragma unroll
+        for (int q = 0; q < F::CPT; ++q) cols[q] = wcol<F>(q, c);
+#pragma unroll
+        for (int i = 0; i < F::RPT; ++i) {
+          const int rr = i * F::TR + r;
+#pragma unroll
+          for (int q = 0; q < F::CPT; ++q)
+            X[i][q] = (rr < nb && cols[q] < w) ? sm.buf[rr * w + cols[q]] : 0.0;
+        }
+        absorb_tile<F>(X, Racc, r, c, cols);
       }
     }
     g = sm.segfl[nb - 1].x;
@@ -396,13 +425,47 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   WarpSmem& sm = all[warp];
+  int dummy = 0;
   while (true) {
     int64_t u = 0;
     if (lane == 0) u = atomicAdd(a.ticket, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= a.n_units) break;
-    process_unit<SLOTS, VEC>(a, geo, sm, u, lane);
+    process_unit<SLOTS, VEC, NoFuse>(a, geo, sm, u, lane, dummy);
   }
+}
+
+// Fused K3 -> K6: heads/tails of own groups with the tails absorbed by a
+// per-warp Householder accumulator (never written to HBM).  Writes one
+// F::W x F::W partial factor per warp to `partials`.
+template <int VEC, class F>
+__global__ void __launch_bounds__(kWarps * 32, F::MINB)
+    k_heads_tails_tsqr(HtDev a, Geo geo, double* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using SM = WarpSmemT<kFusedDoubles>;
+  SM* all = reinterpret_cast<SM*>(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  SM& sm = all[warp];
+  double Racc[F::RR][F::CPT];
+#pragma unroll
+  for (int m = 0; m < F::RR; ++m)
+#pragma unroll
+    for (int q = 0; q < F::CPT; ++q) Racc[m][q] = 0.0;
+  while (true) {
+    int64_t u = 0;
+    if (lane == 0) u = atomicAdd(a.ticket, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= a.n_units) break;
+    process_unit<1, VEC, F>(a, geo, sm, u, lane, Racc);
+  }
+  const int r = lane % F::TR, c = lane / F::TR;
+  double* o = partials + ((int64_t)blockIdx.x * kWarps + warp) * F::W * F::W;
+#pragma unroll
+  for (int m = 0; m < F::RR; ++m)
+#pragma unroll
+    for (int q = 0; q < F::CPT; ++q)
+      if (m * F::TR + r < F::W) o[(m * F::TR + r) * F::W + wcol<F>(q, c)] = Racc[m][q];
 }
 
 // Pre-pass: per unit, the partial sums of its last group if that group is
@@ -468,39 +531,53 @@ __global__ void k_carry_chain(int64_t n_units, int V, const int* __restrict__ co
 }
 
 // K4: joins child summaries into the node's summary rows
-// (figaro.hpp:196-230).  One warp per row; lanes over the row's columns.
-// Child scales are re-read per use instead of kept in a dynamically indexed
-// array (which would live in local memory).
+// (figaro.hpp:196-230).  One thread per summary element (row k, column j):
+// own columns are multiplied by prod_c s_c, child columns are the child's
+// summary row times scale[k] * prod_{d != c} s_d, with the products taken in
+// the reference's order.  The new row scale goes to scale_out (the old one
+// is still being read by other threads of the row).
 __global__ void __launch_bounds__(256) k_join(const __grid_constant__ JoinArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t k = warp; k < a.G; k += nw) {
-    // Lane c (< n_children) loads child c's row index and scale.
-    int my_idx = -1;
-    double my_s = 1.0;
-    if (lane < a.n_children) {
-      my_idx = a.lidx[lane][k];
-      my_s = my_idx >= 0 ? a.child_scale[lane][my_idx] : 0.0;
-    }
-    double all = 1.0;
-    for (int c = 0; c < a.n_children; ++c) all *= __shfl_sync(0xffffffffu, my_s, c);
-    double* dst = a.S + k * a.width;
+  const int64_t total = a.G * a.width;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / a.width;
+    const int j = (int)(e - k * a.width);
+    double* dst = a.S + e;
     const double sk = a.scale[k];
-    for (int c = 0; c < a.n_children; ++c) {
-      const int idx = __shfl_sync(0xffffffffu, my_idx, c);
-      double factor = sk;
-      for (int d = 0; d < a.n_children; ++d) {
-        const double sd = __shfl_sync(0xffffffffu, my_s, d);
-        if (d != c) factor *= sd;
+    if (j < a.own_w) {
+      double all = 1.0;
+      for (int c = 0; c < a.n_children; ++c) {
+        const int idx = a.lidx[c][k];
+        all *= idx >= 0 ? a.child_scale[c][idx] : 0.0;
       }
-      if (idx < 0) continue;
-      const double* src = a.child_S[c] + (int64_t)idx * a.child_w[c];
-      for (int j = lane; j < a.child_w[c]; j += 32)
-        dst[a.child_off[c] + j] = src[j] * factor;
+      *dst *= all;
+      if (j == 0 && a.scale_out) a.scale_out[k] = sk * all;
+      continue;
     }
-    for (int j = lane; j < a.own_w; j += 32) dst[j] *= all;
-    if (lane == 0) a.scale[k] = sk * all;
+    int c = 0;
+    while (c + 1 < a.n_children && j >= a.child_off[c + 1]) ++c;
+    const int idx = a.lidx[c][k];
+    if (idx < 0) continue;
+    double factor = sk;
+    for (int d = 0; d < a.n_children; ++d) {
+      if (d == c) continue;
+      const int id = a.lidx[d][k];
+      factor *= id >= 0 ? a.child_scale[d][id] : 0.0;
+    }
+    *dst = a.child_S[c][(int64_t)idx * a.child_w[c] + (j - a.child_off[c])] * factor;
+  }
+}
+
+// Rows of a node without own columns still need their scale updated.
+__global__ void k_join_scale(const __grid_constant__ JoinArgs a) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.G;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double all = 1.0;
+    for (int c = 0; c < a.n_children; ++c) {
+      const int idx = a.lidx[c][k];
+      all *= idx >= 0 ? a.child_scale[c][idx] : 0.0;
+    }
+    a.scale_out[k] = a.scale[k] * all;
   }
 }
 
@@ -535,10 +612,18 @@ void launch_slots(Context& ctx, const HtDev& d, const Geo& geo) {
 
 }  // namespace
 
-void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
-  if (in.n_seg == 0 || in.n_rows == 0) return;
-  if (in.w > 1024) fail(FG_E_UNSUPPORTED, "heads/tails: more than 1024 columns");
+// Shared set-up of the heads/tails launches: device view, carries of long
+// groups (pre-pass), lane geometry.  `rb_fixed` forces the batch rows.
+struct HtPrep {
   HtDev d{};
+  Geo geo{};
+  DevArray<int> cont, ticket;
+  DevArray<double> val, carry;
+};
+
+static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixed) {
+  HtDev& d = P.d;
+  if (in.w > 1024) fail(FG_E_UNSUPPORTED, "heads/tails: more than 1024 columns");
   d.data = in.data;
   d.ld = in.ld;
   d.w = in.w;
@@ -559,11 +644,13 @@ void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
   d.n_units = ceil_div(in.n_rows, kUnit);
 
   const int V = in.w + (in.weights ? 1 : 0);
-  DevArray<int> cont(d.n_units, ctx.stream);
-  DevArray<double> val, carry;
-  DevArray<int> ticket(1, ctx.stream);
-  ticket.zero();
-  d.ticket = ticket.get();
+  DevArray<int>& cont = P.cont;
+  DevArray<double>& val = P.val;
+  DevArray<double>& carry = P.carry;
+  cont.alloc(d.n_units, ctx.stream);
+  P.ticket.alloc(1, ctx.stream);
+  P.ticket.zero();
+  d.ticket = P.ticket.get();
   if (d.n_units > 1) {
     val.alloc(d.n_units * (size_t)V, ctx.stream);
     carry.alloc((d.n_units + 1) * (size_t)V, ctx.stream);
@@ -582,7 +669,7 @@ void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
     d.carry = carry.get();
   }
   // Vector width, lanes per row-group and rows per batch.
-  Geo geo{};
+  Geo& geo = P.geo;
   const bool aligned = in.w > 0 && in.w % 2 == 0 && in.ld % 2 == 0 &&
                        (reinterpret_cast<uintptr_t>(in.data) % 16 == 0) &&
                        (!in.tails || (in.ldt % 2 == 0 &&
@@ -597,18 +684,87 @@ void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
     if (rb >= geo.G) rb -= rb % geo.G;
     d.rb = std::max(1, rb);
   }
-  if (geo.vec == 2) launch_slots<2>(ctx, d, geo);
-  else launch_slots<1>(ctx, d, geo);
+  if (rb_fixed > 0) d.rb = rb_fixed;
+}
+
+void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
+  if (in.n_seg == 0 || in.n_rows == 0) return;
+  if (in.w > 1024) fail(FG_E_UNSUPPORTED, "heads/tails: more than 1024 columns");
+  HtPrep P;
+  prepare(ctx, in, P, 0);
+  if (P.geo.vec == 2) launch_slots<2>(ctx, P.d, P.geo);
+  else launch_slots<1>(ctx, P.d, P.geo);
+}
+
+namespace {
+using FW4 = WCfg<4, 1, 8, 2>;
+using FW8 = WCfg<8, 2, 8, 2>;
+using FW16 = WCfg<16, 4, 8, 2>;
+using FW32 = WCfg<32, 4, 8, 1>;
+
+template <int VEC, class F>
+int launch_fused(Context& ctx, HtPrep& P, DevArray<double>& partials) {
+  using SM = WarpSmemT<kFusedDoubles>;
+  const size_t smem = sizeof(SM) * kWarps;
+  auto kern = k_heads_tails_tsqr<VEC, F>;
+  FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  int per_sm = 0;
+  FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                        kWarps * 32, smem));
+  int64_t grid = (int64_t)ctx.sm_count * std::max(per_sm, 1);
+  grid = std::max<int64_t>(1, std::min<int64_t>(grid, ceil_div(P.d.n_units, kWarps)));
+  partials.alloc((size_t)grid * kWarps * F::W * F::W, ctx.stream);
+  kern<<<(int)grid, kWarps * 32, smem, ctx.stream>>>(P.d, P.geo, partials.get());
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
+  return (int)(grid * kWarps);
+}
+
+template <class F>
+int fused_for(Context& ctx, const HeadTailArgs& in, DevArray<double>& partials) {
+  HtPrep P;
+  prepare(ctx, in, P, F::B);
+  if (in.w * F::B > kFusedDoubles) fail(FG_E_ARG, "fused tile exceeds shared buffer");
+  return P.geo.vec == 2 ? launch_fused<2, F>(ctx, P, partials)
+                        : launch_fused<1, F>(ctx, P, partials);
+}
+}  // namespace
+
+int fused_width(int w) {
+  if (w <= 0 || w > 32) return 0;
+  return w <= 4 ? 4 : w <= 8 ? 8 : w <= 16 ? 16 : 32;
+}
+
+int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
+                          DevArray<double>& partials) {
+  if (in.n_seg == 0 || in.n_rows == 0 || in.weights) return 0;
+  switch (fused_width(in.w)) {
+    case 4: return fused_for<FW4>(ctx, in, partials);
+    case 8: return fused_for<FW8>(ctx, in, partials);
+    case 16: return fused_for<FW16>(ctx, in, partials);
+    case 32: return fused_for<FW32>(ctx, in, partials);
+    default: fail(FG_E_ARG, "no fused kernel for this width");
+  }
 }
 
 void launch_join(Context& ctx, const JoinArgs& a) {
   if (a.G == 0) return;
   const int threads = 256;
-  int64_t grid = ceil_div(a.G * 32, threads);
-  grid = std::min<int64_t>(grid, (int64_t)ctx.sm_count * 16);
-  k_join<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a);
-  FG_LAUNCHED(ctx);
-  FG_KERNEL_CHECK();
+  const int64_t total = a.G * a.width;
+  if (total > 0) {
+    int64_t grid = ceil_div(total, threads);
+    grid = std::min<int64_t>(grid, (int64_t)ctx.sm_count * 16);
+    k_join<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a);
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+  }
+  if (a.own_w == 0 && a.scale_out) {
+    int64_t grid = std::min<int64_t>(ceil_div(a.G, threads), (int64_t)ctx.sm_count * 16);
+    k_join_scale<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a);
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+  }
 }
 
 }  // namespace fg

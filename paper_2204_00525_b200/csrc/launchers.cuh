@@ -114,13 +114,20 @@ struct HeadTailArgs {
 // Runs the segmented (generalized) head/tail transform.  Needs the max
 // segment size only to decide whether the heavy-segment pre-pass runs.
 void run_heads_tails(Context& ctx, const HeadTailArgs& a);
+// Fused K3 -> K6 for own tails (plain transform, w <= 32): heads/scales as
+// run_heads_tails, tails absorbed per warp; writes count = return value
+// partial factors of fused_width(w) x fused_width(w) to `partials`.
+int fused_width(int w);
+int run_heads_tails_fused(Context& ctx, const HeadTailArgs& a,
+                          DevArray<double>& partials);
 
 struct JoinArgs {
   int64_t G = 0;
   int own_w = 0;
   double* S = nullptr;  // G x width, own head in [0, own_w)
   int64_t width = 0;
-  double* scale = nullptr;  // G
+  double* scale = nullptr;  // G (read)
+  double* scale_out = nullptr;  // G (new scales, must not alias scale)
   int n_children = 0;
   const int* lidx[kMaxChildren];
   const double* child_S[kMaxChildren];
@@ -137,6 +144,10 @@ struct Span {
   int64_t ld;
   int cols;
   int col_begin;
+  // Already factored span (fused kernel): `count` partial W x W factors.
+  const double* partials = nullptr;
+  int count = 0;
+  int W = 0;
 };
 // R (n x n, row-major, device) of the stacked spans, sign-normalised.
 void tsqr(Context& ctx, const std::vector<Span>& spans, int n, double* R_out);

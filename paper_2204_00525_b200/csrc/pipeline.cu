@@ -59,10 +59,12 @@ struct NodeState {
   DevArray<uint64_t> theta, fjs, circ, phi_down, phi_up;
   // summaries
   int64_t width = 0;
-  DevArray<double> S, scale, Sq, scale_q;
+  DevArray<double> S, scale, scale_j, Sq, scale_q;
   const double* sum_S = nullptr;
   const double* sum_scale = nullptr;
   DevArray<double> tails, ptails;
+  DevArray<double> fused;  // partial R factors of the own tails (fused path)
+  int fused_count = 0, fused_W = 0;
 };
 
 struct SpanInfo {
@@ -693,7 +695,8 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     if (!is_leaf) n.S.zero();
     n.scale.alloc(G, st);
     const int64_t n_tails = n.rows - G;
-    if (n.w > 0 && n_tails > 0) n.tails.alloc(n_tails * n.w, st);
+    const bool fuse = opt.fuse && !opt.keep_r0 && fused_width(n.w) > 0 && n_tails > 0;
+    if (n.w > 0 && n_tails > 0 && !fuse) n.tails.alloc(n_tails * n.w, st);
     HeadTailArgs a;
     a.data = n.data;
     a.ld = n.w;
@@ -709,7 +712,12 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     a.tails = n.tails.get();
     a.ldt = n.w;
     a.scales = n.scale.get();
-    run_heads_tails(ctx, a);
+    if (fuse) {
+      n.fused_count = run_heads_tails_fused(ctx, a, n.fused);
+      n.fused_W = fused_width(n.w);
+    } else {
+      run_heads_tails(ctx, a);
+    }
     if (!is_leaf) {
       JoinArgs j{};
       j.G = G;
@@ -717,6 +725,8 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       j.S = n.S.get();
       j.width = n.width;
       j.scale = n.scale.get();
+      n.scale_j.alloc(G, st);
+      j.scale_out = n.scale_j.get();
       j.n_children = (int)n.children.size();
       for (int k = 0; k < j.n_children; ++k) {
         NodeState& c = *nodes[n.children[k]];
@@ -727,6 +737,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
         j.child_off[k] = (int)(lay.sub_begin[n.children[k]] - lay.sub_begin[i]);
       }
       launch_join(ctx, j);
+      std::swap(n.scale, n.scale_j);  // joined scales replace the head scales
     }
     if (!is_root && !is_leaf) {
       n.Sq.alloc(n.P * n.width, st);
@@ -763,7 +774,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   std::vector<SpanInfo>& spans = saved->spans;
   std::function<void(int)> collect = [&](int i) {
     NodeState& n = *nodes[i];
-    if (n.tails.size())
+    if (n.tails.size() || n.fused_count)
       spans.push_back({i, lay.node_offset[i], n.rows - n.grp.G, n.w,
                        n.tails.get()});
     for (int c : n.children) collect(c);
@@ -778,7 +789,14 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   std::vector<Span> tsq;
   for (const auto& s : spans) {
     r0_rows += s.rows;
-    tsq.push_back({s.data, s.rows, s.cols, (int)s.cols, (int)s.col_begin});
+    Span sp{s.data, s.rows, s.cols, (int)s.cols, (int)s.col_begin};
+    NodeState& sn = *nodes[s.node];
+    if (!s.data && sn.fused_count && s.col_begin == lay.node_offset[s.node]) {
+      sp.partials = sn.fused.get();
+      sp.count = sn.fused_count;
+      sp.W = sn.fused_W;
+    }
+    tsq.push_back(sp);
   }
   const int N = (int)lay.total;
   DevArray<double> Rdev;
@@ -821,6 +839,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       n->Sq.release();
       n->tails.release();
       n->ptails.release();
+      n->fused.release();
     }
   }
   if (!opt.keep_r0) spans.clear();
@@ -883,7 +902,7 @@ void fg_options_default(fg_options* o) {
   o->engine = FG_ENGINE_THIN;
   o->memory = FG_MEM_DEVICE;
   o->keep_r0 = 0;
-  o->fuse = 0;
+  o->fuse = 1;
 }
 
 fg_status fg_ctx_create(int32_t device, fg_ctx** out) {

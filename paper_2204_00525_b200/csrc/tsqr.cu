@@ -27,6 +27,7 @@
 #include <string>
 
 #include "launchers.cuh"
+#include "tsqr_warp.cuh"
 
 namespace fg {
 
@@ -68,59 +69,6 @@ __device__ __forceinline__ double group_sum(double x, unsigned mask) {
 #pragma unroll
   for (int o = C::TR / 2; o; o >>= 1) x += __shfl_xor_sync(mask, x, o);
   return x;
-}
-
-// 1/sqrt(q) and 1/q from the MUFU approximations plus two Newton steps
-// (relative error ~1e-16; the IEEE sqrt+div sequence costs ~184 cycles of
-// latency on B200, this ~60).
-__device__ __forceinline__ double fast_rsqrt(double q) {
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-  const double hq = 0.5 * q;
-  r = r * fma(-hq * r, r, 1.5);
-  r = r * fma(-hq * r, r, 1.5);
-  return r;
-}
-__device__ __forceinline__ double fast_rcp(double q) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-  r = r * fma(-q, r, 2.0);
-  r = r * fma(-q, r, 2.0);
-  return r;
-}
-
-// Householder reflector of column k with pivot alpha and tail norm^2 sig in
-// the unnormalised form H = I - tau * u u^T, u = [alpha - beta; x]:
-//   beta = -sign(alpha) * nrm,  nrm = ||(alpha, x)||,
-//   tau  = 1 / (nrm * (nrm + |alpha|)) = t1 * t2,
-// kept as the two bounded factors t1 = 1/nrm and t2 = 1/(nrm + |alpha|)
-// (tau itself overflows for numerically zero columns, nrm < 1e-154).
-// Callers form g = (d * t1) * t2.  t1 = t2 = 0 when the tail is zero
-// (H = I, beta = alpha).
-struct Reflector {
-  double beta, u0, t1, t2;
-};
-__device__ __forceinline__ Reflector make_reflector(double alpha, double sig) {
-  Reflector h;
-  const double q = fma(alpha, alpha, sig);
-  const bool live = sig > 0.0;
-  const double aa = fabs(alpha);
-  double nrm, t1, t2;
-  if (q > 1e-250 && q < 1e250) {
-    // The .ftz approximations flush subnormals: only inside a safe range.
-    t1 = fast_rsqrt(q);
-    nrm = q * t1;
-    t2 = fast_rcp(nrm + aa);
-  } else {
-    nrm = sqrt(q);
-    t1 = 1.0 / nrm;
-    t2 = 1.0 / (nrm + aa);
-  }
-  h.beta = live ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
-  h.u0 = alpha - h.beta;
-  h.t1 = live ? t1 : 0.0;
-  h.t2 = live ? t2 : 0.0;
-  return h;
 }
 
 // Issues the cp.async copies of tile `t` (rows t*B .. t*B+B-1 of the
@@ -272,34 +220,6 @@ __global__ void __launch_bounds__(C::NT)
 // redundantly without divergence, and each lane forms v for its own rows.
 // Partial factors are one per warp.
 
-template <int W_, int CPT_, int RPT_, int MINB_ = 1>
-struct WCfg {
-  static constexpr int W = W_;
-  static constexpr int CPT = CPT_;
-  static constexpr int TC = W / CPT;
-  static constexpr int TR = 32 / TC;
-  static constexpr int RPT = RPT_;
-  static constexpr int B = TR * RPT;
-  static constexpr int RR = (W + TR - 1) / TR;  // accumulator rows per lane
-  static constexpr int WARPS = 8;
-  static constexpr int NT = 32 * WARPS;
-  static constexpr int MINB = MINB_;
-  static constexpr size_t smem_bytes = 0;
-  static_assert(TC * TR == 32, "TC * TR must be a warp");
-};
-
-template <class C>
-__device__ __forceinline__ int wcol(int q, int c) {
-  return (q & 1) ? (q + 1) * C::TC - 1 - c : q * C::TC + c;
-}
-
-template <class C>
-__device__ __forceinline__ double wgroup_sum(double x) {
-#pragma unroll
-  for (int o = C::TR / 2; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
 // Lane (r, c) holds tile rows i*TR + r (i < RPT) of its CPT columns and the
 // accumulator entries R[m*TR + r][col] (m < RR) of the same columns, so the
 // whole column loop is straight-line register code: pivot broadcast by
@@ -351,47 +271,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         X[i][q] = (rp && cols[q] >= lo && cols[q] < hi) ? __ldg(rp + cols[q]) : 0.0;
     }
 
-#pragma unroll
-    for (int k = 0; k < C::W; ++k) {
-      const int qb = k / C::TC;
-      const int within = k % C::TC;
-      const int ck = (qb & 1) ? C::TC - 1 - within : within;
-      const int rk = k % C::TR;   // lane row holding accumulator row k
-      const int mk = k / C::TR;
-      double v[C::RPT];
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int i = 0; i < C::RPT; ++i) {
-        v[i] = __shfl_sync(0xffffffffu, X[i][qb], r + ck * C::TR);
-        if ((i & 3) == 0) s0 = fma(v[i], v[i], s0);
-        else if ((i & 3) == 1) s1 = fma(v[i], v[i], s1);
-        else if ((i & 3) == 2) s2 = fma(v[i], v[i], s2);
-        else s3 = fma(v[i], v[i], s3);
-      }
-      const double sig = wgroup_sum<C>((s0 + s1) + (s2 + s3));
-      const double alpha = __shfl_sync(0xffffffffu, Racc[mk][qb], rk + ck * C::TR);
-      const Reflector h = make_reflector(alpha, sig);
-#pragma unroll
-      for (int q = qb; q < C::CPT; ++q) {
-        const bool act = cols[q] > k;
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-        for (int i = 0; i < C::RPT; ++i) {
-          if ((i & 3) == 0) d0 = fma(v[i], X[i][q], d0);
-          else if ((i & 3) == 1) d1 = fma(v[i], X[i][q], d1);
-          else if ((i & 3) == 2) d2 = fma(v[i], X[i][q], d2);
-          else d3 = fma(v[i], X[i][q], d3);
-        }
-        double d = (d0 + d1) + (d2 + d3);
-        if (r == rk) d = fma(h.u0, Racc[mk][q], d);
-        const double dsum = wgroup_sum<C>(d);  // all lanes shuffle
-        const double f = act ? (dsum * h.t1) * h.t2 : 0.0;
-#pragma unroll
-        for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
-        if (r == rk) Racc[mk][q] = fma(-f, h.u0, Racc[mk][q]);
-      }
-      if (r == rk && c == ck) Racc[mk][qb] = h.beta;
-    }
+    absorb_tile<C>(X, Racc, r, c, cols);
   }
   double* o = out + gw * C::W * C::W;
 #pragma unroll
@@ -560,6 +440,10 @@ void tsqr(Context& ctx, const std::vector<Span>& spans_in, int n,
 
   // Level 0: each span on its own set of persistent CTAs.
   for (const Span& s : spans_in) {
+    if (s.partials) {
+      if (s.count) parts.push_back({s.partials, s.count, s.W, s.cols, s.col_begin});
+      continue;
+    }
     if (s.rows == 0 || s.cols == 0) continue;
     const int W = bucket(s.cols);
     DevArray<double> out;

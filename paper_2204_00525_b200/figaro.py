@@ -329,7 +329,7 @@ def _cstrs(names):
 def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
                  opts: PipelineOptions = PipelineOptions(), keep_r0: bool = False,
                  device: int = 0, fetch_counts: bool = True,
-                 fuse: bool = False) -> PipelineResult:
+                 fuse: bool = True) -> PipelineResult:
     """driver.hpp:47-85 on the GPU.  Host (numpy) relations are copied to the
     device inside the call; torch CUDA relations are used in place and R is
     returned as a CUDA tensor."""

@@ -45,11 +45,11 @@ def to_rels(db, device=True, canonical=False):
     return out
 
 
-def run_gpu(db, device=True, canonical=False, keep_r0=False, assume_reduced=True):
+def run_gpu(db, device=True, canonical=False, keep_r0=False, assume_reduced=True, fuse=True):
     rels = to_rels(db, device, canonical)
     tree = F.build_join_tree(rels, db.root, db.parent)
     res = F.run_pipeline(rels, tree, F.PipelineOptions(assume_reduced=assume_reduced),
-                         keep_r0=keep_r0)
+                         keep_r0=keep_r0, fuse=fuse)
     R = res.factor.r.cpu().numpy() if device else res.factor.r
     return res, R
 
@@ -86,11 +86,11 @@ GOLD = golden_stems("rnd_") + golden_stems("hand_") + golden_stems("big_")
 
 
 @pytest.mark.parametrize("stem", GOLD)
-@pytest.mark.parametrize("device", [True, False])
-def test_golden_pipeline(stem, device):
+@pytest.mark.parametrize("device,fuse", [(True, True), (False, True), (True, False)])
+def test_golden_pipeline(stem, device, fuse):
     db = fgdb.read_fgdb(golden(stem + ".fgdb"))
     ref = fgdb.read_fgrs(golden(stem + ".fgrs"))
-    res, R = run_gpu(db, device=device)
+    res, R = run_gpu(db, device=device, fuse=fuse)
     assert res.r0_rows == ref.r0_rows and res.input_rows == ref.input_rows
     assert r_distance(R, ref.R) <= R_TOL
     check_counts(res, ref)
@@ -134,10 +134,11 @@ def run_ref(db, tmp_path, extra=()):
 
 
 @pytest.mark.parametrize("cfg,scale", [("C2", 0.01), ("C3", 0.002), ("C4", 0.02), ("C5", 0.005)])
-def test_configs_vs_reference(cfg, scale, tmp_path, ref_bin):
+@pytest.mark.parametrize("fuse", [True, False])
+def test_configs_vs_reference(cfg, scale, fuse, tmp_path, ref_bin):
     db = workloads.make(cfg, seed=11, scale=scale)
     ref = run_ref(db, tmp_path)
-    res, R = run_gpu(db)
+    res, R = run_gpu(db, fuse=fuse)
     assert res.r0_rows == ref.r0_rows
     assert r_distance(R, ref.R) <= R_TOL
     check_counts(res, ref)
