@@ -11,6 +11,8 @@
 // counts.hpp:47-62) and exact-division checks (exact_div, counts.hpp:64-71)
 // raise bits in the device status word instead of throwing.  Integer adds
 // commute, so the tables are bit-identical for any launch shape.
+#include <vector>
+
 #include "launchers.cuh"
 
 namespace fg {
@@ -36,24 +38,65 @@ __device__ __forceinline__ void add_chk(uint64_t* slot, uint64_t d,
   if (old + d < old) atomicOr(status, ST_OVERFLOW);
 }
 
+// Warp-aggregated checked add: lanes whose `slot` equals the previous
+// lane's form runs (a segmented shuffle scan sums them); the last lane of a
+// run issues one atomic.  Segments are sorted by own key, so targets keyed by
+// a prefix of it arrive in runs.  Integer sums commute: the table values do
+// not depend on the aggregation.
+__device__ __forceinline__ void add_runs(uint64_t* table, int64_t slot, uint64_t v,
+                                         bool live, unsigned* status) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t prev = __shfl_up_sync(full, slot, 1);
+  const bool prev_live = __shfl_up_sync(full, (int)live, 1) != 0;
+  int head = (lane == 0 || !prev_live || prev != slot || !live) ? 1 : 0;
+  unsigned long long acc = live ? v : 0ull;
+  int ovf = 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(full, acc, o);
+    const int hy = __shfl_up_sync(full, head, o);
+    const int oy = __shfl_up_sync(full, ovf, o);
+    if (lane >= o && !head) {
+      const unsigned long long s2 = acc + y;
+      if (s2 < acc) ovf = 1;
+      acc = s2;
+      ovf |= oy;
+    }
+    if (lane >= o) head |= hy;
+  }
+  const int64_t next = __shfl_down_sync(full, slot, 1);
+  const bool next_live = __shfl_down_sync(full, (int)live, 1) != 0;
+  const bool tail = live && (lane == 31 || !next_live || next != slot);
+  if (tail) {
+    if (ovf) atomicOr(status, ST_OVERFLOW);
+    add_chk(&table[slot], acc, status);
+  }
+}
+
 __global__ void k_theta(const uint64_t* __restrict__ sizes, int64_t G,
                         ChildLinks ch, const int* __restrict__ pidx,
                         uint64_t* phi_down, uint64_t* __restrict__ theta,
                         unsigned* status) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < G;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t t = sizes[k];
-    for (int c = 0; c < ch.n; ++c) {
-      const int q = ch.lidx[c][k];
-      if (q < 0) {
-        atomicOr(status, ST_MISSING_CHILD);
-        t = 0;
-        continue;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t Gw = (G + 31) & ~int64_t(31);  // warp-uniform trip count
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < Gw; k += stride) {
+    const bool live = k < G;
+    uint64_t t = 0;
+    if (live) {
+      t = sizes[k];
+      for (int c = 0; c < ch.n; ++c) {
+        const int q = ch.lidx[c][k];
+        if (q < 0) {
+          atomicOr(status, ST_MISSING_CHILD);
+          t = 0;
+          continue;
+        }
+        t = mul_chk(t, ch.phi_down[c][q], status);
       }
-      t = mul_chk(t, ch.phi_down[c][q], status);
+      theta[k] = t;
     }
-    theta[k] = t;
-    if (pidx) add_chk(&phi_down[pidx[k]], t, status);
+    if (pidx) add_runs(phi_down, live ? pidx[k] : -1, t, live, status);
   }
 }
 
@@ -63,23 +106,54 @@ __global__ void k_fjs(const uint64_t* __restrict__ sizes,
                       const uint64_t* __restrict__ phi_up, ChildLinks ch,
                       uint64_t* __restrict__ fjs, uint64_t* __restrict__ circ,
                       unsigned* status) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < G;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t up = pidx ? phi_up[pidx[k]] : 1ull;
-    const uint64_t f = mul_chk(theta[k], up, status);
-    fjs[k] = f;
-    for (int c = 0; c < ch.n; ++c) {
-      const int q = ch.lidx[c][k];
-      if (q >= 0) add_chk(&ch.phi_up[c][q], f, status);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t Gw = (G + 31) & ~int64_t(31);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < Gw; k += stride) {
+    const bool live = k < G;
+    uint64_t f = 0;
+    if (live) {
+      const uint64_t up = pidx ? phi_up[pidx[k]] : 1ull;
+      f = mul_chk(theta[k], up, status);
+      fjs[k] = f;
+      const uint64_t m = sizes[k];
+      if (m == 0 || f % m != 0) {
+        atomicOr(status, ST_CIRC_INEXACT);
+        circ[k] = 0;
+      } else {
+        circ[k] = f / m;
+      }
     }
-    const uint64_t m = sizes[k];
-    if (m == 0 || f % m != 0) {
-      atomicOr(status, ST_CIRC_INEXACT);
-      circ[k] = 0;
-    } else {
-      circ[k] = f / m;
+    for (int c = 0; c < ch.n; ++c) {
+      const int q = live ? ch.lidx[c][k] : -1;
+      add_runs(ch.phi_up[c], q, f, live && q >= 0, status);
     }
   }
+}
+
+// Scatter-add of fjs into ONE small child table (P <= kPrivMax) through a
+// per-block shared-memory copy: contention stays on-chip (C3's D3 has 1,000
+// keys for 54M F segments).
+constexpr int kPrivMax = 4096;  // 32 KB of static shared memory
+__global__ void k_scatter_priv(const uint64_t* __restrict__ fjs, int64_t G,
+                               const int* __restrict__ lidx, uint64_t* table,
+                               int P, unsigned* status) {
+  __shared__ unsigned long long loc[kPrivMax];
+  __shared__ int ovf;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) loc[i] = 0ull;
+  if (threadIdx.x == 0) ovf = 0;
+  __syncthreads();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < G;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int q = lidx[k];
+    if (q < 0) continue;
+    const unsigned long long v = fjs[k];
+    const unsigned long long old = atomicAdd(&loc[q], v);
+    if (old + v < old) ovf = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ovf) atomicOr(status, ST_OVERFLOW);
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    if (loc[i]) add_chk(&table[i], loc[i], status);
 }
 
 __global__ void k_up_div(uint64_t* __restrict__ phi_up,
@@ -123,14 +197,33 @@ void launch_theta(Context& ctx, const uint64_t* sizes, int64_t G,
 
 void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
                 int64_t G, const int* pidx, const uint64_t* phi_up,
-                const ChildLinks& ch, uint64_t* fjs, uint64_t* circ,
-                unsigned* status) {
+                const ChildLinks& ch, const int64_t* child_P, uint64_t* fjs,
+                uint64_t* circ, unsigned* status) {
   if (G == 0) return;
+  ChildLinks big{};
+  std::vector<int> small;
+  for (int c = 0; c < ch.n; ++c) {
+    if (child_P[c] <= kPrivMax && G > 4 * child_P[c]) {
+      small.push_back(c);
+    } else {
+      big.lidx[big.n] = ch.lidx[c];
+      big.phi_down[big.n] = ch.phi_down[c];
+      big.phi_up[big.n] = ch.phi_up[c];
+      ++big.n;
+    }
+  }
   k_fjs<<<grid_for(ctx, G), kThreads, 0, ctx.stream>>>(sizes, theta, G, pidx,
-                                                       phi_up, ch, fjs, circ,
+                                                       phi_up, big, fjs, circ,
                                                        status);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
+  for (int c : small) {
+    const int grid = (int)std::min<int64_t>(ctx.sm_count * 2, ceil_div(G, kThreads));
+    k_scatter_priv<<<std::max(grid, 1), kThreads, 0, ctx.stream>>>(
+        fjs, G, ch.lidx[c], ch.phi_up[c], (int)child_P[c], status);
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+  }
 }
 
 void launch_up_div(Context& ctx, uint64_t* phi_up, const uint64_t* phi_down,

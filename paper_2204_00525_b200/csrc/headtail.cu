@@ -114,6 +114,34 @@ __device__ __forceinline__ void cp_async(double* dst, const double* src) {
   __pipeline_memcpy_async(dst, src, VEC * sizeof(double));
 }
 
+// Column sums over sorted rows [q0, q1) for this lane's columns: row indices
+// (and weights) are fetched 32 at a time lane-parallel, then each lane walks
+// the chunk with independent loads (no dependent address chain per row).
+__device__ __forceinline__ void chunk_colsum(const HtDev& a, int64_t q0, int64_t q1,
+                                             int col, double& acc, double& nacc,
+                                             bool want_norm, int lane) {
+  const bool weighted = a.weights != nullptr;
+  for (int64_t base = q0; base < q1; base += 32) {
+    const int cnt = (int)(q1 - base < 32 ? q1 - base : 32);
+    int64_t my_row = 0;
+    double my_w = 1.0;
+    if (lane < cnt) {
+      my_row = src_row(a, base + lane);
+      if (weighted) my_w = a.weights[my_row];
+    }
+#pragma unroll 8
+    for (int t = 0; t < cnt; ++t) {
+      const int64_t r = __shfl_sync(0xffffffffu, my_row, t);
+      const double v = weighted ? __shfl_sync(0xffffffffu, my_w, t) : 1.0;
+      if (col >= 0) {
+        const double x = a.data[r * a.ld + col];
+        acc = weighted ? fma(v, x, acc) : acc + x;
+      }
+      if (want_norm) nacc = fma(v, v, nacc);
+    }
+  }
+}
+
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
 template <int SLOTS, int VEC, class SM>
 __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
@@ -164,32 +192,28 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
     const int V = w + (weighted ? 1 : 0);
     const double* cr = chained ? a.carry + u * (int64_t)V : nullptr;
     if (chained && weighted) N = cr[w];
+    if (chained) {
 #pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int pk = cl + geo.L * s;
-      if (pk >= geo.np) continue;
+      for (int s = 0; s < SLOTS; ++s) {
+        const int pk = cl + geo.L * s;
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const int col = VEC * pk + e;
-        if (col >= w) continue;
-        if (chained) {
-          S[s][e] = cr[col];
-        } else {
-          double acc = 0.0;
-          for (int64_t q = gb; q < p0; ++q) {
-            const int64_t rw = src_row(a, q);
-            const double x = a.data[rw * a.ld + col];
-            acc = weighted ? fma(a.weights[rw], x, acc) : acc + x;
-          }
-          S[s][e] = acc;
+        for (int e = 0; e < VEC; ++e) {
+          const int col = VEC * pk + e;
+          if (pk < geo.np && col < w) S[s][e] = cr[col];
         }
       }
-    }
-    if (!chained && weighted) {
-      for (int64_t q = gb; q < p0; ++q) {
-        const double v = a.weights[src_row(a, q)];
-        N = fma(v, v, N);
-      }
+    } else {
+      // Re-read the group's earlier rows (at most kLight of them).
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int pk = cl + geo.L * s;
+          const int col = (pk < geo.np && VEC * pk + e < w) ? VEC * pk + e : -1;
+          double nacc = 0.0;
+          chunk_colsum(a, gb, p0, col, S[s][e], nacc, weighted && s == 0 && e == 0, lane);
+          if (weighted && s == 0 && e == 0) N = nacc;
+        }
     }
   }
 
@@ -488,19 +512,10 @@ __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
     const int64_t q0 = max(b0, p0);
     for (int cb = 0; cb < V; cb += 32) {
       const int col = cb + lane;
-      double s = 0.0;
-      if (col < V) {
-        for (int64_t q = q0; q < p1; ++q) {
-          const int64_t r = src_row(a, q);
-          const double v = weighted ? a.weights[r] : 1.0;
-          if (col < a.w)
-            s = weighted ? fma(v, a.data[r * a.ld + col], s)
-                         : s + a.data[r * a.ld + col];
-          else
-            s = fma(v, v, s);
-        }
-        val[u * (int64_t)V + col] = s;
-      }
+      double s = 0.0, nacc = 0.0;
+      const bool norm_lane = weighted && col == a.w;
+      chunk_colsum(a, q0, p1, col < a.w ? col : -1, s, nacc, norm_lane, lane);
+      if (col < V) val[u * (int64_t)V + col] = norm_lane ? nacc : s;
     }
   }
 }

@@ -87,8 +87,8 @@ void launch_theta(Context& ctx, const uint64_t* sizes, int64_t G,
                   uint64_t* theta, unsigned* status);
 void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
                 int64_t G, const int* pidx, const uint64_t* phi_up,
-                const ChildLinks& ch, uint64_t* fjs, uint64_t* circ,
-                unsigned* status);
+                const ChildLinks& ch, const int64_t* child_P, uint64_t* fjs,
+                uint64_t* circ, unsigned* status);
 void launch_up_div(Context& ctx, uint64_t* phi_up, const uint64_t* phi_down,
                    int64_t P, unsigned* status);
 

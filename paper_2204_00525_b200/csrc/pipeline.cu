@@ -671,9 +671,11 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   }
   for (int i : preorder) {
     NodeState& n = *nodes[i];
+    std::vector<int64_t> child_P;
+    for (int c : n.children) child_P.push_back(nodes[c]->P);
     launch_fjs(ctx, n.sizes.get(), n.theta.get(), n.grp.G,
                n.parent >= 0 ? n.pidx.get() : nullptr, n.phi_up.get(), links(n),
-               n.fjs.get(), n.circ.get(), ctx.status.get());
+               child_P.data(), n.fjs.get(), n.circ.get(), ctx.status.get());
     for (int c : n.children)
       launch_up_div(ctx, nodes[c]->phi_up.get(), nodes[c]->phi_down.get(),
                     nodes[c]->P, ctx.status.get());
