@@ -493,7 +493,10 @@ __global__ void __launch_bounds__(kWarps * 32, F::MINB)
 }
 
 // Pre-pass: per unit, the partial sums of its last group if that group is
-// longer than kLight and continues into the next unit.
+// longer than kLight and continues into the next unit.  Row indices are
+// fetched 32 at a time; lanes sum column pairs with 16-byte loads when the
+// rows are 16-byte aligned.
+template <int VEC>
 __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
                                  double* __restrict__ val) {
   const int lane = threadIdx.x & 31;
@@ -501,6 +504,7 @@ __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool weighted = a.weights != nullptr;
   const int V = a.w + (weighted ? 1 : 0);
+  const int np = (a.w + VEC - 1) / VEC;
   for (int64_t u = warp; u < a.n_units; u += nw) {
     const int64_t p0 = u * kUnit;
     const int64_t p1 = min(p0 + kUnit, a.n_rows);
@@ -510,38 +514,109 @@ __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
     if (lane == 0) cont[u] = c ? (int)g : -1;
     if (!c) continue;
     const int64_t q0 = max(b0, p0);
-    for (int cb = 0; cb < V; cb += 32) {
-      const int col = cb + lane;
-      double s = 0.0, nacc = 0.0;
-      const bool norm_lane = weighted && col == a.w;
-      chunk_colsum(a, q0, p1, col < a.w ? col : -1, s, nacc, norm_lane, lane);
-      if (col < V) val[u * (int64_t)V + col] = norm_lane ? nacc : s;
+    for (int pb = 0; pb < max(np, 1); pb += 32) {
+      const int pk = pb + lane;
+      double s[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) s[e] = 0.0;
+      double nacc = 0.0;
+      for (int64_t base = q0; base < p1; base += 32) {
+        const int cnt = (int)(p1 - base < 32 ? p1 - base : 32);
+        int64_t my_row = 0;
+        double my_w = 1.0;
+        if (lane < cnt) {
+          my_row = src_row(a, base + lane);
+          if (weighted) my_w = a.weights[my_row];
+        }
+#pragma unroll 8
+        for (int t = 0; t < cnt; ++t) {
+          const int64_t r = __shfl_sync(0xffffffffu, my_row, t);
+          const double v = weighted ? __shfl_sync(0xffffffffu, my_w, t) : 1.0;
+          if (pk < np) {
+            const double* src = a.data + r * a.ld + VEC * pk;
+            if (VEC == 2) {
+              const double2 x = *reinterpret_cast<const double2*>(src);
+              s[0] = weighted ? fma(v, x.x, s[0]) : s[0] + x.x;
+              s[VEC - 1] = weighted ? fma(v, x.y, s[VEC - 1]) : s[VEC - 1] + x.y;
+            } else {
+              s[0] = weighted ? fma(v, src[0], s[0]) : s[0] + src[0];
+            }
+          }
+          nacc = fma(v, v, nacc);
+        }
+      }
+      if (pk < np)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          if (VEC * pk + e < a.w) val[u * (int64_t)V + VEC * pk + e] = s[e];
+      if (weighted && pb == 0 && lane == 0) val[u * (int64_t)V + a.w] = nacc;
     }
   }
 }
 
-// Per long group: exclusive scan of unit partial sums over its unit chain;
-// carry[u] receives the prefix of the group's rows before unit u.
-__global__ void k_carry_chain(int64_t n_units, int V, const int* __restrict__ cont,
-                              const double* __restrict__ val,
-                              double* __restrict__ carry) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = warp; u < n_units; u += nw) {
-    const int g = cont[u];
-    if (g < 0 || (u > 0 && cont[u - 1] == g)) continue;  // not a chain start
-    for (int cb = 0; cb < V; cb += 32) {
-      const int col = cb + lane;
-      if (col >= V) continue;
-      double run = 0.0;
-      int64_t x = u;
-      while (x < n_units && cont[x] == g) {
-        run += val[x * (int64_t)V + col];
-        carry[(x + 1) * (int64_t)V + col] = run;
-        ++x;
-      }
+// Carries of long groups: carry[u+1] = sum of val[u'] over the units u' of
+// u's chain (maximal run of equal cont >= 0) up to and including u.  A
+// deterministic three-level segmented scan over units (fixed association):
+//   k_chain_local: per block of kChainBlk units, per column, the in-block
+//                  inclusive run sums (written to carry[u+1]) and the block's
+//                  trailing run sum;
+//   k_chain_top:   sequential over blocks: the carry entering each block;
+//   k_chain_fix:   adds the entering carry to units whose chain started in an
+//                  earlier block.
+constexpr int kChainBlk = 128;
+
+__global__ void k_chain_local(int64_t n_units, int V, const int* __restrict__ cont,
+                              const double* __restrict__ val, double* __restrict__ carry,
+                              double* __restrict__ tailsum, int* __restrict__ starts_in) {
+  const int64_t b = blockIdx.x;
+  const int64_t u0 = b * kChainBlk;
+  const int64_t u1 = min(u0 + kChainBlk, n_units);
+  for (int col = threadIdx.x; col < V; col += blockDim.x) {
+    double run = 0.0;
+    int started = 0;  // a chain starts inside this block before the current unit
+    for (int64_t u = u0; u < u1; ++u) {
+      const int g = cont[u];
+      if (g < 0) { run = 0.0; started = 1; continue; }
+      const bool start = (u == 0) || cont[u - 1] != g;
+      if (start) { run = 0.0; started = 1; }
+      run += val[u * (int64_t)V + col];
+      carry[(u + 1) * (int64_t)V + col] = run;
     }
+    tailsum[b * V + col] = run;
+    if (col == 0) starts_in[b] = started;
+  }
+}
+
+__global__ void k_chain_top(int64_t n_blocks, int64_t n_units, int V,
+                            const int* __restrict__ cont,
+                            const double* __restrict__ tailsum,
+                            const int* __restrict__ starts_in,
+                            double* __restrict__ cin) {
+  for (int col = threadIdx.x; col < V; col += blockDim.x) {
+    double c = 0.0;
+    for (int64_t b = 0; b < n_blocks; ++b) {
+      const int64_t u0 = b * kChainBlk;
+      const bool cont_in = u0 > 0 && cont[u0] >= 0 && cont[u0 - 1] == cont[u0];
+      const double in = cont_in ? c : 0.0;
+      cin[b * V + col] = in;
+      // Carry leaving block b: its trailing run, plus what entered if the
+      // run reaches back to the block start.
+      c = starts_in[b] ? tailsum[b * V + col] : in + tailsum[b * V + col];
+    }
+  }
+}
+
+__global__ void k_chain_fix(int64_t n_units, int V, const int* __restrict__ cont,
+                            const double* __restrict__ cin, double* __restrict__ carry) {
+  const int64_t b = blockIdx.x;
+  const int64_t u0 = b * kChainBlk;
+  const int64_t u1 = min(u0 + kChainBlk, n_units);
+  if (u0 == 0 || cont[u0] < 0 || cont[u0 - 1] != cont[u0]) return;
+  const int g = cont[u0];
+  for (int col = threadIdx.x; col < V; col += blockDim.x) {
+    const double c = cin[b * V + col];
+    for (int64_t u = u0; u < u1 && cont[u] == g; ++u)
+      carry[(u + 1) * (int64_t)V + col] += c;
   }
 }
 
@@ -672,12 +747,30 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     const int threads = 256;
     int64_t grid = ceil_div(d.n_units * 32, threads);
     grid = std::min<int64_t>(grid, (int64_t)ctx.sm_count * 16);
-    k_unit_tail_sums<<<(int)std::max<int64_t>(grid, 1), threads, 0,
-                       ctx.stream>>>(d, cont.get(), val.get());
+    const bool vec2 = in.w % 2 == 0 && in.ld % 2 == 0 &&
+                      reinterpret_cast<uintptr_t>(in.data) % 16 == 0;
+    if (vec2)
+      k_unit_tail_sums<2><<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(
+          d, cont.get(), val.get());
+    else
+      k_unit_tail_sums<1><<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(
+          d, cont.get(), val.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
-    k_carry_chain<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(
-        d.n_units, V, cont.get(), val.get(), carry.get());
+    const int64_t nb = ceil_div(d.n_units, kChainBlk);
+    DevArray<double> tailsum(nb * (size_t)V, ctx.stream), cin(nb * (size_t)V, ctx.stream);
+    DevArray<int> starts(nb, ctx.stream);
+    const int ct = std::min(256, ((V + 31) / 32) * 32);
+    k_chain_local<<<(int)nb, ct, 0, ctx.stream>>>(d.n_units, V, cont.get(), val.get(),
+                                                  carry.get(), tailsum.get(), starts.get());
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+    k_chain_top<<<1, ct, 0, ctx.stream>>>(nb, d.n_units, V, cont.get(), tailsum.get(),
+                                          starts.get(), cin.get());
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+    k_chain_fix<<<(int)nb, ct, 0, ctx.stream>>>(d.n_units, V, cont.get(), cin.get(),
+                                                carry.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
     d.cont = cont.get();
@@ -716,6 +809,9 @@ using FW4 = WCfg<4, 1, 8, 2>;
 using FW8 = WCfg<8, 2, 8, 2>;
 using FW16 = WCfg<16, 4, 8, 2>;
 using FW32 = WCfg<32, 4, 8, 1>;
+using FW12 = WCfg<12, 3, 8, 2>;
+using FW20 = WCfg<20, 5, 8, 1>;
+using FW24 = WCfg<24, 3, 8, 1>;
 
 template <int VEC, class F>
 int launch_fused(Context& ctx, HtPrep& P, DevArray<double>& partials) {
@@ -748,7 +844,9 @@ int fused_for(Context& ctx, const HeadTailArgs& in, DevArray<double>& partials) 
 
 int fused_width(int w) {
   if (w <= 0 || w > 32) return 0;
-  return w <= 4 ? 4 : w <= 8 ? 8 : w <= 16 ? 16 : 32;
+  for (int b : {4, 8, 12, 16, 20, 24, 32})
+    if (w <= b) return b;
+  return 0;
 }
 
 int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
@@ -757,7 +855,10 @@ int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
   switch (fused_width(in.w)) {
     case 4: return fused_for<FW4>(ctx, in, partials);
     case 8: return fused_for<FW8>(ctx, in, partials);
+    case 12: return fused_for<FW12>(ctx, in, partials);
     case 16: return fused_for<FW16>(ctx, in, partials);
+    case 20: return fused_for<FW20>(ctx, in, partials);
+    case 24: return fused_for<FW24>(ctx, in, partials);
     case 32: return fused_for<FW32>(ctx, in, partials);
     default: fail(FG_E_ARG, "no fused kernel for this width");
   }

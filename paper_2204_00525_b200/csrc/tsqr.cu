@@ -302,6 +302,9 @@ using W16 = WCfg<16, 2, 8, 2>;
 using W16b = WCfg<16, 2, 16, 2>;
 using W16c = WCfg<16, 4, 8, 2>;
 using W32 = WCfg<32, 2, 8, 2>;
+using W12 = WCfg<12, 3, 8, 2>;
+using W20 = WCfg<20, 5, 8, 1>;
+using W24 = WCfg<24, 3, 8, 2>;
 using W32c = WCfg<32, 4, 8, 2>;
 using C16 = Cfg<16, 8, 16, 16>;
 using C32 = Cfg<32, 16, 16, 8>;
@@ -316,7 +319,7 @@ int variant(int W) {
 }
 
 int bucket(int w) {
-  for (int b : {4, 8, 16, 32, 64, 128})
+  for (int b : {4, 8, 12, 16, 20, 24, 32, 64, 128})
     if (w <= b) return b;
   return 0;
 }
@@ -361,6 +364,9 @@ Plan plan_for(Context& ctx, int W) {
       return v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
                     : plan_warp<W32>(ctx);
     }
+    case 12: return plan_warp<W12>(ctx);
+    case 20: return plan_warp<W20>(ctx);
+    case 24: return plan_warp<W24>(ctx);
     case 64: return plan_cta<C64>(ctx);
     default: return plan_cta<C128>(ctx);
   }
@@ -387,6 +393,9 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       else k_tsqr_warp<W32><<<grid, W32::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       break;
     }
+    case 12: k_tsqr_warp<W12><<<grid, W12::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 20: k_tsqr_warp<W20><<<grid, W20::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 24: k_tsqr_warp<W24><<<grid, W24::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
     case 64: k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
     default: k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
   }
