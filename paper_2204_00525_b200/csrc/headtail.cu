@@ -492,6 +492,21 @@ __global__ void __launch_bounds__(kWarps * 32, F::MINB)
       if (m * F::TR + r < F::W) o[(m * F::TR + r) * F::W + wcol<F>(q, c)] = Racc[m][q];
 }
 
+// Pre-pass part 1: per unit (one thread each), does its last group continue
+// into the next unit and is it longer than kLight?  Sets *any if so.
+__global__ void k_unit_cont(HtDev a, int* __restrict__ cont, int* any) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.n_units;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = u * kUnit;
+    const int64_t p1 = min(p0 + kUnit, a.n_rows);
+    const int64_t g = seg_of(a.begins, p1 - 1, 0, a.n_seg);
+    const int64_t b0 = a.begins[g], b1 = a.begins[g + 1];
+    const bool c = (b1 > p1) && (b1 - b0 > kLight);
+    cont[u] = c ? (int)g : -1;
+    if (c) *any = 1;
+  }
+}
+
 // Pre-pass: per unit, the partial sums of its last group if that group is
 // longer than kLight and continues into the next unit.  Row indices are
 // fetched 32 at a time; lanes sum column pairs with 16-byte loads when the
@@ -508,12 +523,9 @@ __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
   for (int64_t u = warp; u < a.n_units; u += nw) {
     const int64_t p0 = u * kUnit;
     const int64_t p1 = min(p0 + kUnit, a.n_rows);
-    const int64_t g = seg_of(a.begins, p1 - 1, 0, a.n_seg);
-    const int64_t b0 = a.begins[g], b1 = a.begins[g + 1];
-    const bool c = (b1 > p1) && (b1 - b0 > kLight);
-    if (lane == 0) cont[u] = c ? (int)g : -1;
-    if (!c) continue;
-    const int64_t q0 = max(b0, p0);
+    const int g = cont[u];
+    if (g < 0) continue;
+    const int64_t q0 = max((int64_t)a.begins[g], p0);
     for (int pb = 0; pb < max(np, 1); pb += 32) {
       const int pk = pb + lane;
       double s[VEC];
@@ -567,7 +579,9 @@ constexpr int kChainBlk = 128;
 
 __global__ void k_chain_local(int64_t n_units, int V, const int* __restrict__ cont,
                               const double* __restrict__ val, double* __restrict__ carry,
-                              double* __restrict__ tailsum, int* __restrict__ starts_in) {
+                              double* __restrict__ tailsum, int* __restrict__ starts_in,
+                              const int* any) {
+  if (!*any) return;
   const int64_t b = blockIdx.x;
   const int64_t u0 = b * kChainBlk;
   const int64_t u1 = min(u0 + kChainBlk, n_units);
@@ -591,7 +605,8 @@ __global__ void k_chain_top(int64_t n_blocks, int64_t n_units, int V,
                             const int* __restrict__ cont,
                             const double* __restrict__ tailsum,
                             const int* __restrict__ starts_in,
-                            double* __restrict__ cin) {
+                            double* __restrict__ cin, const int* any) {
+  if (!*any) return;
   for (int col = threadIdx.x; col < V; col += blockDim.x) {
     double c = 0.0;
     for (int64_t b = 0; b < n_blocks; ++b) {
@@ -607,7 +622,9 @@ __global__ void k_chain_top(int64_t n_blocks, int64_t n_units, int V,
 }
 
 __global__ void k_chain_fix(int64_t n_units, int V, const int* __restrict__ cont,
-                            const double* __restrict__ cin, double* __restrict__ carry) {
+                            const double* __restrict__ cin, double* __restrict__ carry,
+                            const int* any) {
+  if (!*any) return;
   const int64_t b = blockIdx.x;
   const int64_t u0 = b * kChainBlk;
   const int64_t u1 = min(u0 + kChainBlk, n_units);
@@ -747,6 +764,12 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     const int threads = 256;
     int64_t grid = ceil_div(d.n_units * 32, threads);
     grid = std::min<int64_t>(grid, (int64_t)ctx.sm_count * 16);
+    DevArray<int> any(1, ctx.stream);
+    any.zero();
+    k_unit_cont<<<(int)std::min<int64_t>(ceil_div(d.n_units, threads), (int64_t)ctx.sm_count * 8),
+                  threads, 0, ctx.stream>>>(d, cont.get(), any.get());
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
     const bool vec2 = in.w % 2 == 0 && in.ld % 2 == 0 &&
                       reinterpret_cast<uintptr_t>(in.data) % 16 == 0;
     if (vec2)
@@ -762,15 +785,16 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     DevArray<int> starts(nb, ctx.stream);
     const int ct = std::min(256, ((V + 31) / 32) * 32);
     k_chain_local<<<(int)nb, ct, 0, ctx.stream>>>(d.n_units, V, cont.get(), val.get(),
-                                                  carry.get(), tailsum.get(), starts.get());
+                                                  carry.get(), tailsum.get(), starts.get(),
+                                                  any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
     k_chain_top<<<1, ct, 0, ctx.stream>>>(nb, d.n_units, V, cont.get(), tailsum.get(),
-                                          starts.get(), cin.get());
+                                          starts.get(), cin.get(), any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
     k_chain_fix<<<(int)nb, ct, 0, ctx.stream>>>(d.n_units, V, cont.get(), cin.get(),
-                                                carry.get());
+                                                carry.get(), any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
     d.cont = cont.get();
@@ -810,7 +834,7 @@ using FW8 = WCfg<8, 2, 8, 2>;
 using FW16 = WCfg<16, 4, 8, 2>;
 using FW32 = WCfg<32, 4, 8, 1>;
 using FW12 = WCfg<12, 3, 8, 2>;
-using FW20 = WCfg<20, 5, 8, 1>;
+using FW20 = WCfg<20, 5, 4, 1>;
 using FW24 = WCfg<24, 3, 8, 1>;
 
 template <int VEC, class F>
@@ -834,9 +858,10 @@ int launch_fused(Context& ctx, HtPrep& P, DevArray<double>& partials) {
 
 template <class F>
 int fused_for(Context& ctx, const HeadTailArgs& in, DevArray<double>& partials) {
+  if (in.w * F::B > kFusedDoubles) return -1;  // caller falls back
   HtPrep P;
   prepare(ctx, in, P, F::B);
-  if (in.w * F::B > kFusedDoubles) fail(FG_E_ARG, "fused tile exceeds shared buffer");
+  if (in.w * F::B > kFusedDoubles) return -1;  // caller falls back
   return P.geo.vec == 2 ? launch_fused<2, F>(ctx, P, partials)
                         : launch_fused<1, F>(ctx, P, partials);
 }
@@ -851,7 +876,7 @@ int fused_width(int w) {
 
 int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
                           DevArray<double>& partials) {
-  if (in.n_seg == 0 || in.n_rows == 0 || in.weights) return 0;
+  if (in.n_seg == 0 || in.n_rows == 0) return 0;
   switch (fused_width(in.w)) {
     case 4: return fused_for<FW4>(ctx, in, partials);
     case 8: return fused_for<FW8>(ctx, in, partials);

@@ -116,7 +116,8 @@ struct HeadTailArgs {
 void run_heads_tails(Context& ctx, const HeadTailArgs& a);
 // Fused K3 -> K6 for own tails (plain transform, w <= 32): heads/scales as
 // run_heads_tails, tails absorbed per warp; writes count = return value
-// partial factors of fused_width(w) x fused_width(w) to `partials`.
+// partial factors of fused_width(w) x fused_width(w) to `partials`;
+// returns -1 (nothing launched) when no fused kernel fits this width.
 int fused_width(int w);
 int run_heads_tails_fused(Context& ctx, const HeadTailArgs& a,
                           DevArray<double>& partials);

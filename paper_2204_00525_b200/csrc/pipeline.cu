@@ -65,6 +65,8 @@ struct NodeState {
   DevArray<double> tails, ptails;
   DevArray<double> fused;  // partial R factors of the own tails (fused path)
   int fused_count = 0, fused_W = 0;
+  DevArray<double> pfused;  // ... and of the project-away tails
+  int pfused_count = 0, pfused_W = 0;
 };
 
 struct SpanInfo {
@@ -717,7 +719,11 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     if (fuse) {
       n.fused_count = run_heads_tails_fused(ctx, a, n.fused);
       n.fused_W = fused_width(n.w);
-    } else {
+    }
+    if (!fuse || n.fused_count < 0) {
+      n.fused_count = 0;
+      if (n.w > 0 && n_tails > 0 && !n.tails.size()) n.tails.alloc(n_tails * n.w, st);
+      a.tails = n.tails.get();
       run_heads_tails(ctx, a);
     }
     if (!is_leaf) {
@@ -744,7 +750,10 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     if (!is_root && !is_leaf) {
       n.Sq.alloc(n.P * n.width, st);
       n.scale_q.alloc(n.P, st);
-      if (n.width > 0 && G > n.P) n.ptails.alloc((G - n.P) * n.width, st);
+      // The generalized (weighted) transform is not fused: measured slower
+      // (C3, width 20) than the separate heads/tails + warp TSQR.
+      const bool pfuse = false;
+      if (n.width > 0 && G > n.P && !pfuse) n.ptails.alloc((G - n.P) * n.width, st);
       HeadTailArgs b;
       b.data = n.S.get();
       b.ld = n.width;
@@ -761,7 +770,16 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       b.tails = n.ptails.get();
       b.ldt = n.width;
       b.scales = n.scale_q.get();
-      run_heads_tails(ctx, b);
+      if (pfuse) {
+        n.pfused_count = run_heads_tails_fused(ctx, b, n.pfused);
+        n.pfused_W = fused_width((int)n.width);
+      }
+      if (!pfuse || n.pfused_count < 0) {
+        n.pfused_count = 0;
+        if (n.width > 0 && G > n.P && !n.ptails.size()) n.ptails.alloc((G - n.P) * n.width, st);
+        b.tails = n.ptails.get();
+        run_heads_tails(ctx, b);
+      }
       n.sum_S = n.Sq.get();
       n.sum_scale = n.scale_q.get();
     } else {
@@ -780,7 +798,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       spans.push_back({i, lay.node_offset[i], n.rows - n.grp.G, n.w,
                        n.tails.get()});
     for (int c : n.children) collect(c);
-    if (n.ptails.size())
+    if (n.ptails.size() || n.pfused_count)
       spans.push_back({i, lay.sub_begin[i], n.grp.G - n.P, n.width,
                        n.ptails.get()});
     if (n.parent < 0 && n.width > 0 && n.grp.G > 0)
@@ -793,10 +811,21 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     r0_rows += s.rows;
     Span sp{s.data, s.rows, s.cols, (int)s.cols, (int)s.col_begin};
     NodeState& sn = *nodes[s.node];
-    if (!s.data && sn.fused_count && s.col_begin == lay.node_offset[s.node]) {
-      sp.partials = sn.fused.get();
-      sp.count = sn.fused_count;
-      sp.W = sn.fused_W;
+    if (!s.data && s.rows > 0) {
+      // Fused spans: own tails are span (node_offset, w); project-away tails
+      // are (subtree_begin, width).  Both can share col_begin, so match the
+      // row count too.
+      const bool own = sn.fused_count && s.col_begin == lay.node_offset[s.node] &&
+                       s.cols == sn.w && s.rows == sn.rows - sn.grp.G;
+      if (own) {
+        sp.partials = sn.fused.get();
+        sp.count = sn.fused_count;
+        sp.W = sn.fused_W;
+      } else if (sn.pfused_count) {
+        sp.partials = sn.pfused.get();
+        sp.count = sn.pfused_count;
+        sp.W = sn.pfused_W;
+      }
     }
     tsq.push_back(sp);
   }
@@ -842,6 +871,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       n->tails.release();
       n->ptails.release();
       n->fused.release();
+      n->pfused.release();
     }
   }
   if (!opt.keep_r0) spans.clear();
