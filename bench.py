@@ -31,23 +31,31 @@ import numpy as np  # noqa: E402
 METRIC = "input tuples/sec to compute R (FP64)"
 REF_BIN = os.path.join(ROOT, "oracle", "_ref", "figaro_ref")
 
-# Algorithmic HBM bytes of the heads/tails phase per config unit:
-# every input data element read once + every tail and final-block element
-# written once.  Computed exactly from the database below.
+# Algorithmic units of the dominant kernel, the own-group
+# heads/tails kernel of each relation (fused with the TSQR leaf when the
+# relation has <= 32 data columns): input rows read once through the sort
+# permutation (8 B per element + 4 B of permutation per row), heads written
+# once, tails written once only when not fused.  FP64 work of the fused
+# kernel: the TSQR flops of the own-tails spans, 2 m w^2 - 2/3 w^3.
 
 
-def heads_tails_bytes(db) -> int:
-    tot = 0
-    ncols = sum(len(r.data_attrs) for r in db.relations)
+def _groups(r) -> int:
+    return np.unique(r.keys, axis=0).shape[0] if r.keys.shape[1] else 1
+
+
+def headtail_units(db):
+    bytes_, flops = 0, 0.0
     for r in db.relations:
         w = len(r.data_attrs)
-        g = np.unique(r.keys, axis=0).shape[0] if r.keys.shape[1] else 1
-        tot += r.rows * w + (r.rows - g) * w
-    # final block (root summary rows x N); 2-relation configs: G_root rows
-    root = db.relations[db.root]
-    groot = np.unique(root.keys, axis=0).shape[0] if root.keys.shape[1] else 1
-    tot += groot * ncols
-    return 8 * tot
+        g = _groups(r)
+        fused = 0 < w <= 32
+        bytes_ += 8 * r.rows * w + 4 * r.rows + 8 * g * w
+        if not fused:
+            bytes_ += 8 * (r.rows - g) * w
+        m = r.rows - g
+        if fused and m > 0:
+            flops += 2.0 * m * w * w - 2.0 / 3.0 * w ** 3
+    return bytes_, flops
 
 
 def tsqr_flops(db) -> float:
@@ -57,14 +65,22 @@ def tsqr_flops(db) -> float:
     fl = 0.0
     for r in db.relations:
         w = len(r.data_attrs)
-        g = np.unique(r.keys, axis=0).shape[0] if r.keys.shape[1] else 1
-        m = r.rows - g
+        m = r.rows - _groups(r)
         fl += 2.0 * m * w * w - 2.0 / 3.0 * w ** 3
-    root = db.relations[db.root]
-    groot = np.unique(root.keys, axis=0).shape[0]
+    groot = _groups(db.relations[db.root])
     fl += 2.0 * groot * ncols ** 2 - 2.0 / 3.0 * ncols ** 3
     fl += 2.0 / 3.0 * ncols ** 3
     return fl
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r1.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["dfma_tflops"]), "measured (profiles/fp64_peak_r1.json, DFMA)"
+    except Exception:
+        return 37.0, "datasheet fallback"
 
 
 def load_peaks():
@@ -249,6 +265,7 @@ def main():
         dist.barrier()
     k0 = ctx.kernel_launches()
     phases = {"group": 0.0, "counts": 0.0, "figaro": 0.0, "post": 0.0}
+    kern = {"headtail": 0.0, "tsqr": 0.0, "headtail_launches": 0}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -260,6 +277,9 @@ def main():
             phases["counts"] += res.seconds_counts
             phases["figaro"] += res.seconds_figaro
             phases["post"] += res.seconds_postprocess
+            kern["headtail"] += res.seconds_headtail_kernels
+            kern["tsqr"] += res.seconds_tsqr_kernels
+            kern["headtail_launches"] += res.headtail_launches
         e1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.kernel_launches() - k0
@@ -300,9 +320,11 @@ def main():
 
     if rank == 0:
         hbm, src = load_peaks()
-        ht_bytes = heads_tails_bytes(db)
-        fig_s = phases["figaro"] / args.steps
-        achieved = ht_bytes / fig_s / 1e9 if fig_s > 0 else 0.0
+        fp64, fsrc = fp64_peak()
+        ht_bytes, ht_flops = headtail_units(db)
+        launches_per_step = max(1, kern["headtail_launches"] // args.steps)
+        ht_s = kern["headtail"] / args.steps          # per step (all launches)
+        achieved = ht_bytes / ht_s / 1e9 if ht_s > 0 else 0.0
         line = {
             "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -312,13 +334,21 @@ def main():
                        "columns": n, "tree": "R1(R2)" if len(db.relations) == 2 else "see workloads",
                        "l2": "inputs larger than L2 (no flush)", "parallelism": f"key-hash x{world}"},
             "phases_ms": {k: v / args.steps * 1e3 for k, v in phases.items()},
-            "roofline": {"kernel": "heads/tails phase (figaro)", "bound": "hbm",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "roofline": {"kernel": "k_heads_tails_tsqr (fused heads/tails -> TSQR leaf; "
+                                   "k_heads_tails when w > 32)",
+                         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
-                         "algorithmic_bytes": ht_bytes, "peak_source": src},
-            "tsqr": {"flops": tsqr_flops(db), "ms": phases["post"] / args.steps * 1e3,
-                     "tflops": tsqr_flops(db) / (phases["post"] / args.steps) / 1e12
-                     if phases["post"] else None},
+                         "algorithmic_bytes_per_launch": ht_bytes / launches_per_step,
+                         "launches_per_step": launches_per_step,
+                         "ms_per_launch": ht_s / launches_per_step * 1e3,
+                         "peak_source": src},
+            "roofline_fp64": {"kernel": "same launches, TSQR work of the own-tails spans",
+                              "achieved": ht_flops / ht_s / 1e12 if ht_s > 0 else 0.0,
+                              "peak": fp64, "unit": "TFLOP/s",
+                              "frac": (ht_flops / ht_s / 1e12) / fp64 if ht_s > 0 else 0.0,
+                              "peak_source": fsrc},
+            "tsqr_stage": {"flops": tsqr_flops(db), "ms": kern["tsqr"] / args.steps * 1e3,
+                           "note": "remaining TSQR work (final block, unfused spans, merges)"},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:

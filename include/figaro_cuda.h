@@ -110,6 +110,10 @@ typedef struct fg_result {
   double seconds_postprocess;
   double seconds_total;   /* whole call incl. host<->device copies         */
   int64_t kernels;        /* kernels launched by this call                  */
+  double seconds_headtail_kernels; /* device time of the heads/tails (or  */
+                          /* fused heads/tails->TSQR) kernels of the call  */
+  double seconds_tsqr_kernels;     /* device time of the TSQR stage        */
+  int64_t headtail_launches;
 } fg_result;
 
 /* Runs validate_join_tree, counts, the FiGaRo transform and the TSQR

@@ -47,7 +47,9 @@ class fg_result(C.Structure):
                 ("r0_rows", C.c_int64), ("seconds_group", C.c_double),
                 ("seconds_counts", C.c_double), ("seconds_figaro", C.c_double),
                 ("seconds_postprocess", C.c_double),
-                ("seconds_total", C.c_double), ("kernels", C.c_int64)]
+                ("seconds_total", C.c_double), ("kernels", C.c_int64),
+                ("seconds_headtail_kernels", C.c_double),
+                ("seconds_tsqr_kernels", C.c_double), ("headtail_launches", C.c_int64)]
 
 
 class fg_block(C.Structure):

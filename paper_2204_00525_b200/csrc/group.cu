@@ -304,48 +304,80 @@ void launch_run_ids(Context& ctx, const uint64_t* sorted, const int* perm,
   FG_KERNEL_CHECK();
 }
 
+// Two-phase grouping so several relations can be sorted before one host
+// synchronisation reads all the group counts.
 template <class KeyT>
-void group_sorted_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
-                    const int* perm_in, GroupOut& out, bool keep_sorted) {
+void group_begin_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
+                   const int* perm_in, GroupOut& out, GroupPending& pend) {
   out.perm.alloc(n, ctx.stream);
-  DevArray<KeyT> sorted(n, ctx.stream);
+  pend.n = n;
+  pend.wide = sizeof(KeyT) == 8;
+  DevArray<KeyT>& sorted = *reinterpret_cast<DevArray<KeyT>*>(
+      pend.wide ? (void*)&pend.sorted64 : (void*)&pend.sorted32);
+  DevArray<KeyT>& uniq = *reinterpret_cast<DevArray<KeyT>*>(
+      pend.wide ? (void*)&pend.uniq64 : (void*)&pend.uniq32);
+  sorted.alloc(n, ctx.stream);
   sort_pairs<KeyT>(ctx, keys, sorted.get(), perm_in, out.perm.get(), n, bits);
-  DevArray<KeyT> uniq(n, ctx.stream);
-  DevArray<int> counts(n + 1, ctx.stream);
-  DevArray<int64_t> nr(1, ctx.stream);
-  run_length<KeyT>(ctx, sorted.get(), n, uniq.get(), counts.get(), nr.get());
-  int64_t G = 0;
-  FG_CUDA(cudaMemcpyAsync(&G, nr.get(), sizeof G, cudaMemcpyDeviceToHost,
-                          ctx.stream));
-  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  uniq.alloc(n, ctx.stream);
+  pend.counts.alloc(n + 1, ctx.stream);
+  pend.nr.alloc(1, ctx.stream);
+  if (n) run_length<KeyT>(ctx, sorted.get(), n, uniq.get(), pend.counts.get(), pend.nr.get());
+  else pend.nr.zero();
+}
+
+void group_finish(Context& ctx, int64_t G, GroupOut& out, GroupPending& pend) {
+  const int64_t n = pend.n;
   out.G = G;
   out.begins.alloc(G + 1, ctx.stream);
-  exclusive_sum_int(ctx, counts.get(), out.begins.get(), G);
+  exclusive_sum_int(ctx, pend.counts.get(), out.begins.get(), G);
   k_set_last<<<1, 1, 0, ctx.stream>>>(out.begins.get(), G, static_cast<int>(n));
   FG_LAUNCHED(ctx);
   out.uniq.alloc(G, ctx.stream);
   if (G) {
-    if constexpr (sizeof(KeyT) == 8) {
-      FG_CUDA(cudaMemcpyAsync(out.uniq.get(), uniq.get(), G * sizeof(uint64_t),
+    if (pend.wide) {
+      FG_CUDA(cudaMemcpyAsync(out.uniq.get(), pend.uniq64.get(), G * sizeof(uint64_t),
                               cudaMemcpyDeviceToDevice, ctx.stream));
     } else {
-      k_widen<<<grid_for(ctx, G), kThreads, 0, ctx.stream>>>(
-          reinterpret_cast<const uint32_t*>(uniq.get()), G, out.uniq.get());
+      k_widen<<<grid_for(ctx, G), kThreads, 0, ctx.stream>>>(pend.uniq32.get(), G,
+                                                            out.uniq.get());
       FG_LAUNCHED(ctx);
       FG_KERNEL_CHECK();
     }
   }
-  if (keep_sorted) {
-    if constexpr (sizeof(KeyT) == 8) {
-      out.sorted = std::move(sorted);
+  if (pend.keep_sorted) {
+    if (pend.wide) {
+      out.sorted = std::move(pend.sorted64);
     } else {
       out.sorted.alloc(n, ctx.stream);
-      k_widen<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(
-          reinterpret_cast<const uint32_t*>(sorted.get()), n, out.sorted.get());
+      k_widen<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(pend.sorted32.get(), n,
+                                                            out.sorted.get());
       FG_LAUNCHED(ctx);
       FG_KERNEL_CHECK();
     }
   }
+  pend = GroupPending();
+}
+
+void group_begin(Context& ctx, const uint64_t* keys, int64_t n, int bits,
+                 const int* perm_in, GroupOut& out, GroupPending& pend) {
+  group_begin_t<uint64_t>(ctx, keys, n, bits, perm_in, out, pend);
+}
+void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
+                   const int* perm_in, GroupOut& out, GroupPending& pend) {
+  group_begin_t<uint32_t>(ctx, keys, n, bits, perm_in, out, pend);
+}
+
+template <class KeyT>
+void group_sorted_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
+                    const int* perm_in, GroupOut& out, bool keep_sorted) {
+  GroupPending pend;
+  pend.keep_sorted = keep_sorted;
+  group_begin_t<KeyT>(ctx, keys, n, bits, perm_in, out, pend);
+  int64_t G = 0;
+  FG_CUDA(cudaMemcpyAsync(&G, pend.nr.get(), sizeof G, cudaMemcpyDeviceToHost,
+                          ctx.stream));
+  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  group_finish(ctx, G, out, pend);
 }
 
 void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,

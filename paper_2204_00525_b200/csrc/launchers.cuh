@@ -42,6 +42,22 @@ struct GroupOut {
 };
 void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
                   const int* perm_in, GroupOut& out, bool keep_sorted = false);
+// Split form: begin (sort + run-length, no sync) for several inputs, one
+// sync reading every pend.nr, then finish with the counts.
+struct GroupPending {
+  int64_t n = 0;
+  bool wide = true;
+  bool keep_sorted = false;
+  DevArray<uint64_t> sorted64, uniq64;
+  DevArray<uint32_t> sorted32, uniq32;
+  DevArray<int> counts;
+  DevArray<int64_t> nr;  // device: number of runs
+};
+void group_begin(Context& ctx, const uint64_t* keys, int64_t n, int bits,
+                 const int* perm_in, GroupOut& out, GroupPending& pend);
+void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
+                   const int* perm_in, GroupOut& out, GroupPending& pend);
+void group_finish(Context& ctx, int64_t G, GroupOut& out, GroupPending& pend);
 // Same with 32-bit packed keys (own keys of <= 32 significant bits).
 void group_sorted32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
                     const int* perm_in, GroupOut& out, bool keep_sorted = false);

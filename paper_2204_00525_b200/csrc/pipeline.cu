@@ -414,6 +414,36 @@ struct Trace {
   }
 };
 
+// Event pairs bracketing individual launches (per-kernel device time).
+struct KernelTimer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  cudaStream_t st;
+  explicit KernelTimer(cudaStream_t s) : st(s) {}
+  ~KernelTimer() {
+    for (auto& e : ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  }
+  void begin() {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    ev.push_back({a, b});
+    cudaEventRecord(a, st);
+  }
+  void end() { cudaEventRecord(ev.back().second, st); }
+  double seconds() const {
+    double s = 0;
+    for (auto& e : ev) {
+      float t = 0;
+      cudaEventElapsedTime(&t, e.first, e.second);
+      s += t * 1e-3;
+    }
+    return s;
+  }
+};
+
 struct Events {
   cudaEvent_t e[6];
   Events() { for (auto& x : e) cudaEventCreate(&x); }
@@ -464,6 +494,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
 
   Trace tr;
   Events ev;
+  KernelTimer kt_ht(st), kt_tsqr(st);
   FG_CUDA(cudaEventRecord(ev.e[0], st));
 
   // Inputs on the device.
@@ -547,9 +578,14 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       }
   }
 
-  // ---- K1: own-key grouping per relation
-  for (auto& np : nodes) {
-    NodeState& n = *np;
+  // ---- K1: own-key grouping per relation.  All sorts are enqueued first;
+  // one synchronisation reads every relation's group count.
+  std::vector<GroupPending> pend(nodes.size());
+  std::vector<DevArray<uint32_t>> pk32(nodes.size());
+  std::vector<DevArray<uint64_t>> pk64(nodes.size());
+  std::vector<DevArray<int>> iotas(nodes.size());
+  for (size_t ni = 0; ni < nodes.size(); ++ni) {
+    NodeState& n = *nodes[ni];
     n.own = make_spec(n.key_attr, code,
                       [&](int a) {
                         return (int)(std::find(n.key_attr.begin(),
@@ -559,66 +595,102 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
                       &n.own_bits, "relation " + n.name);
     if (n.own_bits <= 32 && !n.has_sel) {
       // Narrow packed keys: 8 instead of 12 bytes per element per radix pass.
-      DevArray<uint32_t> pk(n.rows, st);
-      DevArray<int> iota(n.rows, st);
-      launch_pack_keys<uint32_t>(ctx, n.keys, n.rows, n.n_key, n.own, pk.get(),
-                                 iota.get());
-      group_sorted32(ctx, pk.get(), n.rows, n.own_bits, iota.get(), n.grp);
+      pk32[ni].alloc(n.rows, st);
+      iotas[ni].alloc(n.rows, st);
+      launch_pack_keys<uint32_t>(ctx, n.keys, n.rows, n.n_key, n.own, pk32[ni].get(),
+                                 iotas[ni].get());
+      group_begin32(ctx, pk32[ni].get(), n.rows, n.own_bits, iotas[ni].get(), n.grp,
+                    pend[ni]);
     } else {
-      DevArray<uint64_t> pk(n.rows, st);
-      DevArray<int> iota;
+      pk64[ni].alloc(n.rows, st);
       if (n.rows) {
         if (n.has_sel) {
           k_pack_sel<<<grid1d(ctx, n.rows), 256, 0, st>>>(n.keys, n.n_key,
                                                           n.sel.get(), n.rows,
-                                                          n.own, pk.get());
+                                                          n.own, pk64[ni].get());
           FG_LAUNCHED(ctx);
           FG_KERNEL_CHECK();
         } else {
-          iota.alloc(n.rows, st);
+          iotas[ni].alloc(n.rows, st);
           launch_pack_keys<uint64_t>(ctx, n.keys, n.rows, n.n_key, n.own,
-                                     pk.get(), iota.get());
+                                     pk64[ni].get(), iotas[ni].get());
         }
       }
-      group_sorted(ctx, pk.get(), n.rows, n.own_bits,
-                   n.has_sel ? n.sel.get() : iota.get(), n.grp);
+      group_begin(ctx, pk64[ni].get(), n.rows, n.own_bits,
+                  n.has_sel ? n.sel.get() : iotas[ni].get(), n.grp, pend[ni]);
     }
-    n.sizes.alloc(n.grp.G, st);
-    launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
+  }
+  {
+    std::vector<int64_t> Gs(nodes.size(), 0);
+    for (size_t ni = 0; ni < nodes.size(); ++ni)
+      FG_CUDA(cudaMemcpyAsync(&Gs[ni], pend[ni].nr.get(), sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+    FG_CUDA(cudaStreamSynchronize(st));
+    for (size_t ni = 0; ni < nodes.size(); ++ni) {
+      NodeState& n = *nodes[ni];
+      group_finish(ctx, Gs[ni], n.grp, pend[ni]);
+      pk32[ni].release();
+      pk64[ni].release();
+      iotas[ni].release();
+      n.sizes.alloc(n.grp.G, st);
+      launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
+    }
   }
   tr.mark("own grouping");
   // Parent-key grouping of own segments (the std::map regroupings of
-  // counts.hpp:121-130 and figaro.hpp:236-239).
-  for (auto& np : nodes) {
-    NodeState& n = *np;
-    if (n.parent < 0) continue;
-    int pbits = 0;
-    n.par = make_spec(n.pattr, code,
-                      [&](int a) {
-                        const int f = (int)(std::find(n.key_attr.begin(),
-                                                      n.key_attr.end(), a) -
-                                            n.key_attr.begin());
-                        return n.own.shift[f];
-                      },
-                      &pbits, "relation " + n.name + " (parent key)");
-    const int64_t G = n.grp.G;
-    DevArray<uint64_t> ppk(G, st);
-    launch_project(ctx, n.grp.uniq.get(), G, n.par, ppk.get());
-    DevArray<int> iota(G, st);
-    launch_iota(ctx, iota.get(), G);
-    GroupOut pg;
-    group_sorted(ctx, ppk.get(), G, pbits, iota.get(), pg, true);
-    n.P = pg.G;
-    n.pa_perm = std::move(pg.perm);
-    n.pa_begins = std::move(pg.begins);
-    n.upk = std::move(pg.uniq);
-    n.pidx.alloc(G, st);
-    DevArray<int> flags(G, st), scan(G, st);
-    launch_run_ids(ctx, pg.sorted.get(), n.pa_perm.get(), G, flags.get(),
-                   scan.get(), n.pidx.get());
-    if (n.children.empty() && n.P != G)
-      fail(FG_E_INTEGRITY, "relation " + n.name +
-                               ": leaf keys do not match its parent attributes");
+  // counts.hpp:121-130 and figaro.hpp:236-239), batched like K1.
+  {
+    std::vector<GroupPending> ppend(nodes.size());
+    std::vector<GroupOut> pgs(nodes.size());
+    std::vector<DevArray<uint64_t>> ppks(nodes.size());
+    std::vector<DevArray<int>> piotas(nodes.size());
+    for (size_t ni = 0; ni < nodes.size(); ++ni) {
+      NodeState& n = *nodes[ni];
+      if (n.parent < 0) continue;
+      int pbits = 0;
+      n.par = make_spec(n.pattr, code,
+                        [&](int a) {
+                          const int f = (int)(std::find(n.key_attr.begin(),
+                                                        n.key_attr.end(), a) -
+                                              n.key_attr.begin());
+                          return n.own.shift[f];
+                        },
+                        &pbits, "relation " + n.name + " (parent key)");
+      const int64_t G = n.grp.G;
+      ppks[ni].alloc(G, st);
+      launch_project(ctx, n.grp.uniq.get(), G, n.par, ppks[ni].get());
+      piotas[ni].alloc(G, st);
+      launch_iota(ctx, piotas[ni].get(), G);
+      ppend[ni].keep_sorted = true;
+      group_begin(ctx, ppks[ni].get(), G, pbits, piotas[ni].get(), pgs[ni], ppend[ni]);
+    }
+    std::vector<int64_t> Ps(nodes.size(), 0);
+    bool any = false;
+    for (size_t ni = 0; ni < nodes.size(); ++ni)
+      if (nodes[ni]->parent >= 0) {
+        FG_CUDA(cudaMemcpyAsync(&Ps[ni], ppend[ni].nr.get(), sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, st));
+        any = true;
+      }
+    if (any) FG_CUDA(cudaStreamSynchronize(st));
+    for (size_t ni = 0; ni < nodes.size(); ++ni) {
+      NodeState& n = *nodes[ni];
+      if (n.parent < 0) continue;
+      const int64_t G = n.grp.G;
+      GroupOut& pg = pgs[ni];
+      group_finish(ctx, Ps[ni], pg, ppend[ni]);
+      n.P = pg.G;
+      n.pa_perm = std::move(pg.perm);
+      n.pa_begins = std::move(pg.begins);
+      n.upk = std::move(pg.uniq);
+      n.pidx.alloc(G, st);
+      DevArray<int> flags(G, st), scan(G, st);
+      launch_run_ids(ctx, pg.sorted.get(), n.pa_perm.get(), G, flags.get(),
+                     scan.get(), n.pidx.get());
+      if (n.children.empty() && n.P != G)
+        fail(FG_E_INTEGRITY, "relation " + n.name +
+                                 ": leaf keys do not match its parent attributes");
+    }
   }
   tr.mark("parent grouping");
   // Edge lookups: own segment of i -> parent-key index of child c.
@@ -716,6 +788,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     a.tails = n.tails.get();
     a.ldt = n.w;
     a.scales = n.scale.get();
+    kt_ht.begin();
     if (fuse) {
       n.fused_count = run_heads_tails_fused(ctx, a, n.fused);
       n.fused_W = fused_width(n.w);
@@ -726,6 +799,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       a.tails = n.tails.get();
       run_heads_tails(ctx, a);
     }
+    kt_ht.end();
     if (!is_leaf) {
       JoinArgs j{};
       j.G = G;
@@ -778,7 +852,9 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
         n.pfused_count = 0;
         if (n.width > 0 && G > n.P && !n.ptails.size()) n.ptails.alloc((G - n.P) * n.width, st);
         b.tails = n.ptails.get();
+        kt_ht.begin();
         run_heads_tails(ctx, b);
+        kt_ht.end();
       }
       n.sum_S = n.Sq.get();
       n.sum_scale = n.scale_q.get();
@@ -836,7 +912,9 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     Rdev.alloc((size_t)N * N, st);
     Rd = Rdev.get();
   }
+  kt_tsqr.begin();
   tsqr(ctx, tsq, N, Rd);
+  kt_tsqr.end();
   tr.mark("tsqr enqueue");
   FG_CUDA(cudaEventRecord(ev.e[5], st));
   if (opt.memory == FG_MEM_HOST && N > 0)
@@ -858,6 +936,9 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     res->seconds_postprocess = ev.ms(4, 5);
     res->seconds_total = ev.ms(0, 5);
     res->kernels = ctx.launches - launches0;
+    res->seconds_headtail_kernels = kt_ht.seconds();
+    res->seconds_tsqr_kernels = kt_tsqr.seconds();
+    res->headtail_launches = (int64_t)kt_ht.ev.size();
   }
   // Keep the inspection state; drop the bulky buffers unless R0 is wanted.
   saved->have_r0 = opt.keep_r0 != 0;

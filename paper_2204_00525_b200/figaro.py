@@ -315,6 +315,9 @@ class PipelineResult:
     seconds_postprocess: float
     seconds_total: float
     kernels: int
+    seconds_headtail_kernels: float = 0.0
+    seconds_tsqr_kernels: float = 0.0
+    headtail_launches: int = 0
     counts: Optional[List[NodeCounts]] = None
     r0: Optional[List[OutSpan]] = None
 
@@ -378,7 +381,10 @@ def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
         r0_rows=res.r0_rows, input_rows=res.input_rows, data_columns=res.data_columns,
         seconds_group=res.seconds_group, seconds_counts=res.seconds_counts,
         seconds_figaro=res.seconds_figaro, seconds_postprocess=res.seconds_postprocess,
-        seconds_total=res.seconds_total, kernels=res.kernels)
+        seconds_total=res.seconds_total, kernels=res.kernels,
+        seconds_headtail_kernels=res.seconds_headtail_kernels,
+        seconds_tsqr_kernels=res.seconds_tsqr_kernels,
+        headtail_launches=res.headtail_launches)
     if fetch_counts:
         out.counts = [fetch_node_counts(ctx, i, rels[i], tree) for i in range(len(rels))]
     if keep_r0:
