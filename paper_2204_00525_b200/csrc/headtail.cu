@@ -638,53 +638,61 @@ __global__ void k_chain_fix(int64_t n_units, int V, const int* __restrict__ cont
 }
 
 // K4: joins child summaries into the node's summary rows
-// (figaro.hpp:196-230).  One thread per summary element (row k, column j):
-// own columns are multiplied by prod_c s_c, child columns are the child's
-// summary row times scale[k] * prod_{d != c} s_d, with the products taken in
-// the reference's order.  The new row scale goes to scale_out (the old one
-// is still being read by other threads of the row).
-__global__ void __launch_bounds__(256) k_join(const __grid_constant__ JoinArgs a) {
+// (figaro.hpp:196-230), in two passes.  k_join_rows (thread per row): the
+// product of the child scales `all`, the per-child factors
+// scale[k] * prod_{d != c} s_d in the reference's product order, and the new
+// row scale (scale_out).  k_join_elems (thread per summary element): own
+// columns times `all`, child columns = child summary row times its factor.
+__global__ void __launch_bounds__(256) k_join_rows(const __grid_constant__ JoinArgs a,
+                                                   double* __restrict__ fac) {
+  const int nc = a.n_children;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.G;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double sc[kMaxChildren];
+    double all = 1.0;
+#pragma unroll
+    for (int c = 0; c < kMaxChildren; ++c) {
+      sc[c] = 0.0;
+      if (c < nc) {
+        const int idx = a.lidx[c][k];
+        sc[c] = idx >= 0 ? a.child_scale[c][idx] : 0.0;
+        all *= sc[c];
+      }
+    }
+    const double sk = a.scale[k];
+    if (a.scale_out) a.scale_out[k] = sk * all;
+    double* f = fac + k * (nc + 1);
+    f[nc] = all;
+#pragma unroll
+    for (int c = 0; c < kMaxChildren; ++c) {
+      if (c >= nc) break;
+      double x = sk;
+#pragma unroll
+      for (int d = 0; d < kMaxChildren; ++d)
+        if (d != c && d < nc) x *= sc[d];
+      f[c] = x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_join_elems(const __grid_constant__ JoinArgs a,
+                                                    const double* __restrict__ fac) {
+  const int nc = a.n_children;
   const int64_t total = a.G * a.width;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = e / a.width;
     const int j = (int)(e - k * a.width);
-    double* dst = a.S + e;
-    const double sk = a.scale[k];
+    const double* f = fac + k * (nc + 1);
     if (j < a.own_w) {
-      double all = 1.0;
-      for (int c = 0; c < a.n_children; ++c) {
-        const int idx = a.lidx[c][k];
-        all *= idx >= 0 ? a.child_scale[c][idx] : 0.0;
-      }
-      *dst *= all;
-      if (j == 0 && a.scale_out) a.scale_out[k] = sk * all;
+      a.S[e] *= f[nc];
       continue;
     }
     int c = 0;
-    while (c + 1 < a.n_children && j >= a.child_off[c + 1]) ++c;
+    while (c + 1 < nc && j >= a.child_off[c + 1]) ++c;
     const int idx = a.lidx[c][k];
     if (idx < 0) continue;
-    double factor = sk;
-    for (int d = 0; d < a.n_children; ++d) {
-      if (d == c) continue;
-      const int id = a.lidx[d][k];
-      factor *= id >= 0 ? a.child_scale[d][id] : 0.0;
-    }
-    *dst = a.child_S[c][(int64_t)idx * a.child_w[c] + (j - a.child_off[c])] * factor;
-  }
-}
-
-// Rows of a node without own columns still need their scale updated.
-__global__ void k_join_scale(const __grid_constant__ JoinArgs a) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.G;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    double all = 1.0;
-    for (int c = 0; c < a.n_children; ++c) {
-      const int idx = a.lidx[c][k];
-      all *= idx >= 0 ? a.child_scale[c][idx] : 0.0;
-    }
-    a.scale_out[k] = a.scale[k] * all;
+    a.S[e] = a.child_S[c][(int64_t)idx * a.child_w[c] + (j - a.child_off[c])] * f[c];
   }
 }
 
@@ -892,17 +900,15 @@ int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
 void launch_join(Context& ctx, const JoinArgs& a) {
   if (a.G == 0) return;
   const int threads = 256;
+  DevArray<double> fac(a.G * (a.n_children + 1), ctx.stream);
+  int64_t grid = std::min<int64_t>(ceil_div(a.G, threads), (int64_t)ctx.sm_count * 16);
+  k_join_rows<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a, fac.get());
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
   const int64_t total = a.G * a.width;
   if (total > 0) {
-    int64_t grid = ceil_div(total, threads);
-    grid = std::min<int64_t>(grid, (int64_t)ctx.sm_count * 16);
-    k_join<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a);
-    FG_LAUNCHED(ctx);
-    FG_KERNEL_CHECK();
-  }
-  if (a.own_w == 0 && a.scale_out) {
-    int64_t grid = std::min<int64_t>(ceil_div(a.G, threads), (int64_t)ctx.sm_count * 16);
-    k_join_scale<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a);
+    grid = std::min<int64_t>(ceil_div(total, threads), (int64_t)ctx.sm_count * 16);
+    k_join_elems<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a, fac.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
   }

@@ -296,6 +296,10 @@ __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
 
 using C64 = Cfg<64, 32, 8, 16>;
 using C128 = Cfg<128, 32, 8, 8>;
+using C64a = Cfg<64, 32, 8, 8>;
+using C64b = Cfg<64, 16, 16, 8>;
+using C128a = Cfg<128, 32, 8, 4>;
+using C128b = Cfg<128, 16, 16, 4>;
 using W4 = WCfg<4, 1, 8, 2>;
 using W8 = WCfg<8, 2, 8, 2>;
 using W16 = WCfg<16, 2, 8, 2>;
@@ -312,9 +316,11 @@ using C32 = Cfg<32, 16, 16, 8>;
 // Kernel variant per width (FG_TSQR_W16 / FG_TSQR_W32 = warp | warpb |
 // warpc | cta) -- a tuning knob; the default is the measured best.
 int variant(int W) {
-  const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32" : "FG_TSQR_X");
+  const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32"
+                         : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128" : "FG_TSQR_X");
   if (!e) return W == 16 ? 2 : W == 32 ? 3 : 0;  // measured best (tsqr_sweep.py)
   const std::string v = e;
+  if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : 0;
   return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : 0;
 }
 
@@ -367,8 +373,14 @@ Plan plan_for(Context& ctx, int W) {
     case 12: return plan_warp<W12>(ctx);
     case 20: return plan_warp<W20>(ctx);
     case 24: return plan_warp<W24>(ctx);
-    case 64: return plan_cta<C64>(ctx);
-    default: return plan_cta<C128>(ctx);
+    case 64: {
+      const int v = variant(64);
+      return v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx) : plan_cta<C64>(ctx);
+    }
+    default: {
+      const int v = variant(128);
+      return v == 1 ? plan_cta<C128a>(ctx) : v == 2 ? plan_cta<C128b>(ctx) : plan_cta<C128>(ctx);
+    }
   }
 }
 
@@ -396,8 +408,20 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
     case 12: k_tsqr_warp<W12><<<grid, W12::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
     case 20: k_tsqr_warp<W20><<<grid, W20::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
     case 24: k_tsqr_warp<W24><<<grid, W24::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 64: k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
-    default: k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 64: {
+      const int v = variant(64);
+      if (v == 1) k_tsqr<C64a><<<grid, C64a::NT, C64a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 2) k_tsqr<C64b><<<grid, C64b::NT, C64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      break;
+    }
+    default: {
+      const int v = variant(128);
+      if (v == 1) k_tsqr<C128a><<<grid, C128a::NT, C128a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 2) k_tsqr<C128b><<<grid, C128b::NT, C128b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      break;
+    }
   }
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
@@ -418,6 +442,8 @@ struct Partial {
 int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_unit,
            DevArray<double>& out) {
   const Plan p = plan_for(ctx, W);
+  // A unit must absorb more rows than a factor has, or merges cannot shrink.
+  tiles_per_unit = std::max<int64_t>(tiles_per_unit, 2 * ceil_div(W, p.B));
   int64_t rows = 0;
   for (auto& s : segs) {
     s.row0 = rows;
