@@ -241,3 +241,23 @@ def test_cpp_facade_on_reference_types():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "PASS" in out.stdout
+
+
+@pytest.mark.parametrize("w1,w2", [(12, 20), (24, 5), (32, 3), (1, 33), (7, 9), (64, 2)])
+@pytest.mark.parametrize("fuse", [True, False])
+def test_widths_cover_every_kernel_shape(w1, w2, fuse, tmp_path, ref_bin):
+    """2-relation joins whose widths hit each fused / TSQR bucket (4..128),
+    odd widths (scalar path) and long groups (carry chains)."""
+    rng = np.random.default_rng(w1 * 100 + w2)
+    rels = []
+    for i, w in enumerate((w1, w2)):
+        keys = np.concatenate([rng.integers(0, 300, 4000), np.full(900, 7)]).reshape(-1, 1)
+        rng.shuffle(keys)
+        data = rng.standard_normal((keys.shape[0], w)) * rng.uniform(0.1, 10.0, w)
+        rels.append(fgdb.RelationData(f"R{i}", ["k"], [f"c{i}_{j}" for j in range(w)],
+                                      keys.astype(np.int64), data))
+    db = fgdb.Database(rels, 0, [-1, 0])
+    ref = run_ref(db, tmp_path)
+    res, R = run_gpu(db, fuse=fuse)
+    assert r_distance(R, ref.R) <= R_TOL
+    check_counts(res, ref)
