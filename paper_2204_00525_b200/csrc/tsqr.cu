@@ -305,6 +305,9 @@ using W8 = WCfg<8, 2, 8, 2>;
 using W16 = WCfg<16, 2, 8, 2>;
 using W16b = WCfg<16, 2, 16, 2>;
 using W16c = WCfg<16, 4, 8, 2>;
+using W16d = WCfg<16, 4, 4, 3>;
+using W16e = WCfg<16, 4, 16, 1>;
+using W16f = WCfg<16, 8, 4, 2>;
 using W32 = WCfg<32, 2, 8, 2>;
 using W12 = WCfg<12, 3, 8, 2>;
 using W20 = WCfg<20, 5, 8, 1>;
@@ -321,7 +324,8 @@ int variant(int W) {
   if (!e) return W == 16 ? 2 : W == 32 ? 3 : 0;  // measured best (tsqr_sweep.py)
   const std::string v = e;
   if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : 0;
-  return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : 0;
+  return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : v == "warpd" ? 4
+         : v == "warpe" ? 5 : v == "warpf" ? 6 : 0;
 }
 
 int bucket(int w) {
@@ -363,7 +367,9 @@ Plan plan_for(Context& ctx, int W) {
     case 16: {
       const int v = variant(16);
       return v == 1 ? plan_warp<W16b>(ctx) : v == 2 ? plan_warp<W16c>(ctx)
-             : v == 3 ? plan_cta<C16>(ctx) : plan_warp<W16>(ctx);
+             : v == 3 ? plan_cta<C16>(ctx) : v == 4 ? plan_warp<W16d>(ctx)
+             : v == 5 ? plan_warp<W16e>(ctx) : v == 6 ? plan_warp<W16f>(ctx)
+             : plan_warp<W16>(ctx);
     }
     case 32: {
       const int v = variant(32);
@@ -395,6 +401,9 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       if (v == 1) k_tsqr_warp<W16b><<<grid, W16b::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 2) k_tsqr_warp<W16c><<<grid, W16c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 3) k_tsqr<C16><<<grid, C16::NT, C16::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 4) k_tsqr_warp<W16d><<<grid, W16d::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 5) k_tsqr_warp<W16e><<<grid, W16e::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 6) k_tsqr_warp<W16f><<<grid, W16f::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else k_tsqr_warp<W16><<<grid, W16::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       break;
     }
