@@ -83,6 +83,21 @@ def fp64_peak():
         return 37.0, "datasheet fallback"
 
 
+def ncu_traffic(prefix: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/ncu_traffic_r1.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic_r1.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        for k, v in d.items():
+            if prefix in k:
+                return v["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -337,7 +352,10 @@ def main():
             "roofline": {"kernel": "k_heads_tails_tsqr (fused heads/tails -> TSQR leaf; "
                                    "k_heads_tails when w > 32)",
                          "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
+                         "frac": achieved / hbm,
+                         "traffic": ncu_traffic("k_heads_tails_tsqr<2, WCfg<16")
+                         if args.config == "C2" else None,
+                         "traffic_source": "profiles/ncu_traffic_r1.json (ncu --set full, C2)",
                          "algorithmic_bytes_per_launch": ht_bytes / launches_per_step,
                          "launches_per_step": launches_per_step,
                          "ms_per_launch": ht_s / launches_per_step * 1e3,
