@@ -27,6 +27,8 @@
 
 #include <type_traits>
 
+#include <string>
+
 #include "launchers.cuh"
 #include "tsqr_warp.cuh"
 
@@ -64,6 +66,7 @@ struct HtDev {
   const double* carry;   // per unit: incoming carry (V values), valid when
                          // cont[u-1] == first group of u
   int* ticket;
+  const int* ufirst;     // per unit: group of its first row (or null)
 };
 
 __device__ __forceinline__ int64_t src_row(const HtDev& a, int64_t p) {
@@ -89,10 +92,11 @@ struct WarpSmemT {
   double hco[kMaxRB];     // head coefficient at a group's last row
   double wt[kMaxRB];      // generalized weights
   int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
+  unsigned char startf[kMaxRB];  // 1 where a group starts inside the batch
   const double* rowptr[kMaxRB];
 };
 using WarpSmem = WarpSmemT<kSmemDoubles>;
-constexpr int kFusedDoubles = 1024;  // one TSQR tile of tails (B x w)
+constexpr int kFusedDoubles = 1280;  // one TSQR tile of tails (B x ls)
 
 __device__ __forceinline__ double fast_rsqrt_d(double q) {
   double r;
@@ -105,8 +109,9 @@ __device__ __forceinline__ double fast_rsqrt_d(double q) {
 
 // Lane geometry: the warp is split into G row-groups of L lanes; lane cl of
 // a group owns column packets cl + L*s (s < SLOTS) of VEC doubles each.
+// ls: row stride of the staged batch in shared memory (doubles).
 struct Geo {
-  int vec, np, L, G;
+  int vec, np, L, G, ls;
 };
 
 template <int VEC>
@@ -153,7 +158,7 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
   const int g = lane / geo.L, cl = lane % geo.L;
   for (int rr = g; rr < nb; rr += geo.G) {
     const double* src = sm.rowptr[rr];
-    double* dst = sm.buf + rr * a.w;
+    double* dst = sm.buf + rr * geo.ls;
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
       const int pk = cl + geo.L * s;
@@ -174,7 +179,7 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
   const bool weighted = a.weights != nullptr;
   const int64_t p0 = u * kUnit;
   const int64_t p1 = min(p0 + kUnit, a.n_rows);
-  int64_t g = seg_of(a.begins, p0, 0, a.n_seg);
+  int64_t g = a.ufirst ? (int64_t)a.ufirst[u] : seg_of(a.begins, p0, 0, a.n_seg);
   const int grp = lane / geo.L, cl = lane % geo.L;
 
   // Running prefix (per owned column) carried into the next batch.
@@ -220,18 +225,32 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
   for (int64_t pb = p0; pb < p1; pb += a.rb) {
     const int nb = (int)(p1 - pb < (int64_t)a.rb ? p1 - pb : (int64_t)a.rb);
     if (w > 0) stage_rows<SLOTS, VEC>(a, geo, sm, pb, nb, lane);
+    // Group starts inside the batch (groups g+1 .. g+nb can start here):
+    // flagged in shared memory, then each row's group is g plus a ballot
+    // prefix count -- one level of loads instead of a binary search per row.
+    for (int i = lane; i < kMaxRB; i += 32) sm.startf[i] = 0;
+    __syncwarp();
+    for (int i = lane; i < nb; i += 32) {
+      const int64_t gi = g + 1 + i;
+      if (gi < a.n_seg) {
+        const int64_t b = a.begins[gi];
+        if (b < pb + nb) sm.startf[b - pb] = 1;
+      }
+    }
+    __syncwarp();
+    int64_t gcur = g;
     // Row metadata and coefficients, one row per lane.
-    const int64_t g_hi = (g + nb + 1 < a.n_seg) ? g + nb + 1 : a.n_seg;
     for (int base = 0; base < nb; base += 32) {
       const int rr = base + lane;
       const bool live = rr < nb;
-      int64_t sg = g;
+      const unsigned smask = __ballot_sync(0xffffffffu, live && sm.startf[rr]);
+      int64_t sg = gcur + __popc(smask & ((2u << lane) - 1u));
+      gcur += __popc(smask);
       int64_t jj = 0, m = 1;
       double v = 1.0;
       int fl = 0;
       if (live) {
         const int64_t p = pb + rr;
-        sg = seg_of(a.begins, p, g, g_hi);
         const int64_t b0 = a.begins[sg];
         const int64_t b1 = a.begins[sg + 1];
         jj = p - b0;
@@ -314,7 +333,7 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         const int fl = sm.segfl[rr].y;
         const double vw = sm.wt[rr];
         if (fl & 1) has_start = 1;
-        const double* row = sm.buf + rr * w;
+        const double* row = sm.buf + rr * geo.ls;
 #pragma unroll
         for (int s = 0; s < SLOTS; ++s) {
           const int pk = cl + geo.L * s;
@@ -377,7 +396,7 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
           hrow = a.heads + hi * a.ldh;
           hc = sm.hco[rr];
         }
-        const double* row = sm.buf + rr * w;
+        const double* row = sm.buf + rr * geo.ls;
 #pragma unroll
         for (int s = 0; s < SLOTS; ++s) {
           const int pk = cl + geo.L * s;
@@ -431,7 +450,7 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
           const int rr = i * F::TR + r;
 #pragma unroll
           for (int q = 0; q < F::CPT; ++q)
-            X[i][q] = (rr < nb && cols[q] < w) ? sm.buf[rr * w + cols[q]] : 0.0;
+            X[i][q] = (rr < nb && cols[q] < w) ? sm.buf[rr * geo.ls + cols[q]] : 0.0;
         }
         absorb_tile<F>(X, Racc, r, c, cols);
       }
@@ -494,7 +513,8 @@ __global__ void __launch_bounds__(kWarps * 32, F::MINB)
 
 // Pre-pass part 1: per unit (one thread each), does its last group continue
 // into the next unit and is it longer than kLight?  Sets *any if so.
-__global__ void k_unit_cont(HtDev a, int* __restrict__ cont, int* any) {
+__global__ void k_unit_cont(HtDev a, int* __restrict__ cont, int* __restrict__ ufirst,
+                            int* any) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.n_units;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p0 = u * kUnit;
@@ -504,6 +524,9 @@ __global__ void k_unit_cont(HtDev a, int* __restrict__ cont, int* any) {
     const bool c = (b1 > p1) && (b1 - b0 > kLight);
     cont[u] = c ? (int)g : -1;
     if (c) *any = 1;
+    // First group of the next unit: g again unless a group starts at p1.
+    if (u + 1 < a.n_units) ufirst[u + 1] = (int)(b1 == p1 ? g + 1 : g);
+    if (u == 0) ufirst[0] = 0;
   }
 }
 
@@ -732,7 +755,7 @@ void launch_slots(Context& ctx, const HtDev& d, const Geo& geo) {
 struct HtPrep {
   HtDev d{};
   Geo geo{};
-  DevArray<int> cont, ticket;
+  DevArray<int> cont, ticket, ufirst;
   DevArray<double> val, carry;
 };
 
@@ -763,6 +786,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   DevArray<double>& val = P.val;
   DevArray<double>& carry = P.carry;
   cont.alloc(d.n_units, ctx.stream);
+  P.ufirst.alloc(d.n_units, ctx.stream);
   P.ticket.alloc(1, ctx.stream);
   P.ticket.zero();
   d.ticket = P.ticket.get();
@@ -775,7 +799,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     DevArray<int> any(1, ctx.stream);
     any.zero();
     k_unit_cont<<<(int)std::min<int64_t>(ceil_div(d.n_units, threads), (int64_t)ctx.sm_count * 8),
-                  threads, 0, ctx.stream>>>(d, cont.get(), any.get());
+                  threads, 0, ctx.stream>>>(d, cont.get(), P.ufirst.get(), any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
     const bool vec2 = in.w % 2 == 0 && in.ld % 2 == 0 &&
@@ -807,6 +831,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     FG_KERNEL_CHECK();
     d.cont = cont.get();
     d.carry = carry.get();
+    d.ufirst = P.ufirst.get();
   }
   // Vector width, lanes per row-group and rows per batch.
   Geo& geo = P.geo;
@@ -824,7 +849,18 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     if (rb >= geo.G) rb -= rb % geo.G;
     d.rb = std::max(1, rb);
   }
+  geo.ls = in.w;
   if (rb_fixed > 0) d.rb = rb_fixed;
+}
+
+// Row stride for a fused tile: the TSQR tile load has TR lanes reading TR
+// rows of the same TC adjacent columns; ls = TC (mod 2 TC) puts those rows on
+// disjoint bank groups (2 wavefronts per 8-byte load instead of TR).
+template <class F>
+int fused_stride(int w) {
+  int ls = w;
+  while (ls % (2 * F::TC) != F::TC % (2 * F::TC)) ++ls;
+  return ls + (ls & 1);  // double2 staging needs an even stride
 }
 
 void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
@@ -840,6 +876,7 @@ namespace {
 using FW4 = WCfg<4, 1, 8, 2>;
 using FW8 = WCfg<8, 2, 8, 2>;
 using FW16 = WCfg<16, 4, 8, 2>;
+using FW16r = WCfg<16, 4, 8, 2, 1>;
 using FW32 = WCfg<32, 4, 8, 1>;
 using FW12 = WCfg<12, 3, 8, 2>;
 using FW20 = WCfg<20, 5, 4, 1>;
@@ -866,10 +903,11 @@ int launch_fused(Context& ctx, HtPrep& P, DevArray<double>& partials) {
 
 template <class F>
 int fused_for(Context& ctx, const HeadTailArgs& in, DevArray<double>& partials) {
-  if (in.w * F::B > kFusedDoubles) return -1;  // caller falls back
+  const int ls = fused_stride<F>(in.w);
+  if (ls * F::B > kFusedDoubles) return -1;  // caller falls back
   HtPrep P;
   prepare(ctx, in, P, F::B);
-  if (in.w * F::B > kFusedDoubles) return -1;  // caller falls back
+  P.geo.ls = ls;
   return P.geo.vec == 2 ? launch_fused<2, F>(ctx, P, partials)
                         : launch_fused<1, F>(ctx, P, partials);
 }
@@ -889,7 +927,11 @@ int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
     case 4: return fused_for<FW4>(ctx, in, partials);
     case 8: return fused_for<FW8>(ctx, in, partials);
     case 12: return fused_for<FW12>(ctx, in, partials);
-    case 16: return fused_for<FW16>(ctx, in, partials);
+    case 16: {
+      const char* e = getenv("FG_FUSED_W16");
+      if (e && std::string(e) == "roll") return fused_for<FW16r>(ctx, in, partials);
+      return fused_for<FW16>(ctx, in, partials);
+    }
     case 20: return fused_for<FW20>(ctx, in, partials);
     case 24: return fused_for<FW24>(ctx, in, partials);
     case 32: return fused_for<FW32>(ctx, in, partials);

@@ -308,6 +308,7 @@ using W16c = WCfg<16, 4, 8, 2>;
 using W16d = WCfg<16, 4, 4, 3>;
 using W16e = WCfg<16, 4, 16, 1>;
 using W16f = WCfg<16, 8, 4, 2>;
+using W16g = WCfg<16, 4, 8, 2, 1>;
 using W32 = WCfg<32, 2, 8, 2>;
 using W12 = WCfg<12, 3, 8, 2>;
 using W20 = WCfg<20, 5, 8, 1>;
@@ -325,7 +326,7 @@ int variant(int W) {
   const std::string v = e;
   if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : 0;
   return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : v == "warpd" ? 4
-         : v == "warpe" ? 5 : v == "warpf" ? 6 : 0;
+         : v == "warpe" ? 5 : v == "warpf" ? 6 : v == "warpg" ? 7 : 0;
 }
 
 int bucket(int w) {
@@ -369,6 +370,7 @@ Plan plan_for(Context& ctx, int W) {
       return v == 1 ? plan_warp<W16b>(ctx) : v == 2 ? plan_warp<W16c>(ctx)
              : v == 3 ? plan_cta<C16>(ctx) : v == 4 ? plan_warp<W16d>(ctx)
              : v == 5 ? plan_warp<W16e>(ctx) : v == 6 ? plan_warp<W16f>(ctx)
+             : v == 7 ? plan_warp<W16g>(ctx)
              : plan_warp<W16>(ctx);
     }
     case 32: {
@@ -404,6 +406,7 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       else if (v == 4) k_tsqr_warp<W16d><<<grid, W16d::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 5) k_tsqr_warp<W16e><<<grid, W16e::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 6) k_tsqr_warp<W16f><<<grid, W16f::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 7) k_tsqr_warp<W16g><<<grid, W16g::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else k_tsqr_warp<W16><<<grid, W16::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       break;
     }

@@ -59,7 +59,10 @@ __device__ __forceinline__ Reflector make_reflector(double alpha, double sig) {
   return h;
 }
 
-template <int W_, int CPT_, int RPT_, int MINB_ = 1>
+// ROLL_ = 1 keeps only the column-block loop unrolled in absorb_tile (the
+// TC steps inside a block run as a loop): ~1/TC of the code, for kernels
+// whose straight-line body overflows the instruction cache.
+template <int W_, int CPT_, int RPT_, int MINB_ = 1, int ROLL_ = 0>
 struct WCfg {
   static constexpr int W = W_;
   static constexpr int CPT = CPT_;
@@ -71,6 +74,7 @@ struct WCfg {
   static constexpr int WARPS = 8;
   static constexpr int NT = 32 * WARPS;
   static constexpr int MINB = MINB_;
+  static constexpr int ROLL = ROLL_;
   static constexpr size_t smem_bytes = 0;
   static_assert(TC * TR == 32, "TC * TR must be a warp");
 };
@@ -87,54 +91,91 @@ __device__ __forceinline__ double wgroup_sum(double x) {
   return x;
 }
 
+// One column step k of absorb_tile; QB (the column block) is compile-time,
+// the position inside the block may be a run-time value.
+template <class C, int QB>
+__device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
+                                            double (&Racc)[C::RR][C::CPT],
+                                            int r, int c, const int (&cols)[C::CPT],
+                                            int within) {
+  const int k = QB * C::TC + within;
+  const int ck = (QB & 1) ? C::TC - 1 - within : within;
+  const int rk = k % C::TR;   // lane row holding accumulator row k
+  const int mk = k / C::TR;
+  double v[C::RPT];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int i = 0; i < C::RPT; ++i) {
+    v[i] = __shfl_sync(0xffffffffu, X[i][QB], r + ck * C::TR);
+    if ((i & 3) == 0) s0 = fma(v[i], v[i], s0);
+    else if ((i & 3) == 1) s1 = fma(v[i], v[i], s1);
+    else if ((i & 3) == 2) s2 = fma(v[i], v[i], s2);
+    else s3 = fma(v[i], v[i], s3);
+  }
+  const double sig = wgroup_sum<C>((s0 + s1) + (s2 + s3));
+  // Racc[mk][q] for a possibly run-time mk: a select chain over RR rows.
+  auto racc = [&](int q) {
+    double x = Racc[0][q];
+#pragma unroll
+    for (int m = 1; m < C::RR; ++m)
+      if (mk == m) x = Racc[m][q];
+    return x;
+  };
+  const double alpha = __shfl_sync(0xffffffffu, racc(QB), rk + ck * C::TR);
+  const Reflector h = make_reflector(alpha, sig);
+#pragma unroll
+  for (int q = QB; q < C::CPT; ++q) {
+    const bool act = cols[q] > k;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i) {
+      if ((i & 3) == 0) d0 = fma(v[i], X[i][q], d0);
+      else if ((i & 3) == 1) d1 = fma(v[i], X[i][q], d1);
+      else if ((i & 3) == 2) d2 = fma(v[i], X[i][q], d2);
+      else d3 = fma(v[i], X[i][q], d3);
+    }
+    double d = (d0 + d1) + (d2 + d3);
+    const double rq = racc(q);
+    if (r == rk) d = fma(h.u0, rq, d);
+    const double dsum = wgroup_sum<C>(d);  // all lanes shuffle
+    const double f = act ? (dsum * h.t1) * h.t2 : 0.0;
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
+    if (r == rk) {
+      const double nr = (q == QB && c == ck) ? h.beta : fma(-f, h.u0, rq);
+#pragma unroll
+      for (int m = 0; m < C::RR; ++m)
+        if (mk == m) Racc[m][q] = nr;
+    }
+  }
+}
+
+template <class C, int QB>
+__device__ __forceinline__ void absorb_blocks(double (&X)[C::RPT][C::CPT],
+                                              double (&Racc)[C::RR][C::CPT],
+                                              int r, int c, const int (&cols)[C::CPT]) {
+  if constexpr (QB < C::CPT) {
+    if constexpr (C::ROLL) {
+#pragma unroll 1
+      for (int within = 0; within < C::TC; ++within)
+        absorb_step<C, QB>(X, Racc, r, c, cols, within);
+    } else {
+#pragma unroll
+      for (int within = 0; within < C::TC; ++within)
+        absorb_step<C, QB>(X, Racc, r, c, cols, within);
+    }
+    absorb_blocks<C, QB + 1>(X, Racc, r, c, cols);
+  }
+}
+
 // Absorbs one B x W tile (X, lane layout above) into the accumulator rows
 // Racc: the W column steps of the structured Householder QR of [R; X]
-// (postprocess.hpp:35-64 shape, LAPACK tpqrt), straight-line register code.
+// (postprocess.hpp:35-64 shape, LAPACK tpqrt), register code.
 template <class C>
 __device__ __forceinline__ void absorb_tile(double (&X)[C::RPT][C::CPT],
                                             double (&Racc)[C::RR][C::CPT],
                                             int r, int c, const int (&cols)[C::CPT]) {
-#pragma unroll
-  for (int k = 0; k < C::W; ++k) {
-    const int qb = k / C::TC;
-    const int within = k % C::TC;
-    const int ck = (qb & 1) ? C::TC - 1 - within : within;
-    const int rk = k % C::TR;   // lane row holding accumulator row k
-    const int mk = k / C::TR;
-    double v[C::RPT];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < C::RPT; ++i) {
-      v[i] = __shfl_sync(0xffffffffu, X[i][qb], r + ck * C::TR);
-      if ((i & 3) == 0) s0 = fma(v[i], v[i], s0);
-      else if ((i & 3) == 1) s1 = fma(v[i], v[i], s1);
-      else if ((i & 3) == 2) s2 = fma(v[i], v[i], s2);
-      else s3 = fma(v[i], v[i], s3);
-    }
-    const double sig = wgroup_sum<C>((s0 + s1) + (s2 + s3));
-    const double alpha = __shfl_sync(0xffffffffu, Racc[mk][qb], rk + ck * C::TR);
-    const Reflector h = make_reflector(alpha, sig);
-#pragma unroll
-    for (int q = qb; q < C::CPT; ++q) {
-      const bool act = cols[q] > k;
-      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-      for (int i = 0; i < C::RPT; ++i) {
-        if ((i & 3) == 0) d0 = fma(v[i], X[i][q], d0);
-        else if ((i & 3) == 1) d1 = fma(v[i], X[i][q], d1);
-        else if ((i & 3) == 2) d2 = fma(v[i], X[i][q], d2);
-        else d3 = fma(v[i], X[i][q], d3);
-      }
-      double d = (d0 + d1) + (d2 + d3);
-      if (r == rk) d = fma(h.u0, Racc[mk][q], d);
-      const double dsum = wgroup_sum<C>(d);  // all lanes shuffle
-      const double f = act ? (dsum * h.t1) * h.t2 : 0.0;
-#pragma unroll
-      for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
-      if (r == rk) Racc[mk][q] = fma(-f, h.u0, Racc[mk][q]);
-    }
-    if (r == rk && c == ck) Racc[mk][qb] = h.beta;
-  }
+  absorb_blocks<C, 0>(X, Racc, r, c, cols);
 }
 
 }  // namespace fg

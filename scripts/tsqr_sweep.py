@@ -18,7 +18,7 @@ def bench(blocks, n, reps=5):
         torch.cuda.synchronize(); best = min(best, time.perf_counter() - t)
     return best, R
 
-for var in ["warpc", "warpd", "warpe", "warpf", "warpb"]:
+for var in ["warpc", "warpg", "warpe"]:
     os.environ["FG_TSQR_W16"] = var
     t, R = bench([(x16, 0)], 16)
     fl = 2 * 15e6 * 256
