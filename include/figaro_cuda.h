@@ -51,7 +51,8 @@ enum {
   FG_E_SIZE = 5,        /* figaro::size_error (u64 count overflow)        */
   FG_E_EMPTY_JOIN = 6,  /* figaro::empty_join_error                       */
   FG_E_UNSUPPORTED = 7, /* input shape this build does not handle         */
-  FG_E_CUDA = 8         /* CUDA runtime / launch failure                  */
+  FG_E_CUDA = 8,        /* CUDA runtime / launch failure                  */
+  FG_E_RANK = 9         /* figaro::rank_error (singular R in recover_q)   */
 };
 
 typedef struct fg_ctx fg_ctx;
@@ -197,6 +198,39 @@ typedef struct fg_block {
 } fg_block;
 FG_API fg_status fg_tsqr(fg_ctx* ctx, int32_t n_blocks, const fg_block* blocks,
                   int32_t n, double* R_out);
+
+/* ---- join rows and Q = A R^-1 (the steps after R) ---------------------- */
+
+/* The join rows in the reference's depth-first order (for_each_join_row,
+ * join.hpp:47-92): root rows in input order, then for every node in
+ * pre-order the rows of that relation whose parent-shared key equals its
+ * parent's current row's, in input order.  Relations are used as given (not
+ * canonicalised, not reduced); dangling tuples yield no rows.  A row has
+ * n = sum of n_data values in the pre-order column layout (make_layout,
+ * join_tree.hpp:186-219).  More than `cap` rows -> FG_E_SIZE (join.hpp:77-79;
+ * the reference's default cap is 1,000,000).  `memory` says where keys/data,
+ * R, A_out and Q_out live (FG_MEM_DEVICE | FG_MEM_HOST); output buffers hold
+ * rows x n doubles, row-major -- size them with fg_join_size. */
+
+/* Number of join rows (for_each_join_row with an empty sink, join.hpp:63). */
+FG_API fg_status fg_join_size(fg_ctx* ctx, int32_t n_rel, const fg_relation* rels,
+                              int32_t root, const int32_t* parent, int32_t memory,
+                              uint64_t cap, int64_t* rows);
+/* A = the dense join (materialize_join, join.hpp:96-112). */
+FG_API fg_status fg_materialize_join(fg_ctx* ctx, int32_t n_rel,
+                                     const fg_relation* rels, int32_t root,
+                                     const int32_t* parent, int32_t memory,
+                                     uint64_t cap, double* A_out, int64_t* rows);
+/* Q = A R^{-1} row by row (recover_q, postprocess.hpp:293-321): R is the
+ * n x n upper-triangular factor (row-major); q solves q R = a by forward
+ * substitution in the reference's operation order.  |R_ii| <= 1e-12 ||R||_F
+ * -> FG_E_RANK before any work.  A_out (the streamed a_row) may be NULL;
+ * with Q_out and A_out both NULL only the checks run and *rows is set.
+ * n <= 128. */
+FG_API fg_status fg_recover_q(fg_ctx* ctx, int32_t n_rel, const fg_relation* rels,
+                              int32_t root, const int32_t* parent, int32_t memory,
+                              uint64_t cap, const double* R, double* A_out,
+                              double* Q_out, int64_t* rows);
 
 #ifdef __cplusplus
 }

@@ -561,6 +561,86 @@ def run_pipeline(rels: List[Relation], root: int, parent: Sequence[int],
                           sum(r.rows for r in rels), layout.total, counts, r0)
 
 
+# --------------------------------------------------------------------------
+# join.hpp / recover_q
+
+
+class rank_error(error):
+    """error.hpp:43-46"""
+
+
+DEFAULT_JOIN_CAP = 1_000_000  # join.hpp:25
+
+
+def join_rows(rels: List[Relation], tree: JoinTree, cap: int = DEFAULT_JOIN_CAP) -> np.ndarray:
+    """for_each_join_row (join.hpp:47-92) collected into a dense array:
+    root rows in input order, then per pre-order node the rows matching the
+    parent's current row (EdgeIndex keeps insertion order, join.hpp:29-38);
+    dangling tuples yield nothing; more than `cap` rows -> size_error."""
+    layout = Layout(rels, tree)
+    index = []
+    for i, rel in enumerate(rels):
+        m: Dict[tuple, List[int]] = {}
+        if i != tree.root:
+            for r in range(rel.rows):
+                m.setdefault(project_key(rel.key_tuple(r), rel.key_attrs,
+                                         tree.parent_attrs[i]), []).append(r)
+        index.append(m)
+    out: List[np.ndarray] = []
+    row = np.zeros(layout.total)
+    cur = [0] * len(rels)
+
+    def emit(depth):
+        if depth == len(tree.preorder):
+            if len(out) + 1 > cap:
+                raise size_error(f"join row cap exceeded ({cap} rows)")
+            out.append(row.copy())
+            return
+        node = tree.preorder[depth]
+        rel = rels[node]
+        off = layout.node_offset[node]
+        if node == tree.root:
+            cand = range(rel.rows)
+        else:
+            p = tree.parent[node]
+            probe = project_key(rels[p].key_tuple(cur[p]), rels[p].key_attrs,
+                                tree.parent_attrs[node])
+            cand = index[node].get(probe, [])
+        for r in cand:
+            cur[node] = r
+            row[off:off + rel.data.shape[1]] = rel.data[r]
+            emit(depth + 1)
+
+    emit(0)
+    return np.array(out).reshape(len(out), layout.total)
+
+
+def recover_q(rels: List[Relation], tree: JoinTree, R: np.ndarray,
+              cap: int = DEFAULT_JOIN_CAP) -> Tuple[np.ndarray, np.ndarray]:
+    """recover_q (postprocess.hpp:293-321): (A, Q) with q R = a solved per row
+    by forward substitution in the reference's operation order (vectorised
+    over rows; each element sees the same scalar operations)."""
+    n = R.shape[1]
+    if n != Layout(rels, tree).total:
+        raise error("recover_q: factor size does not match column layout")
+    s = 0.0
+    for i in range(R.shape[0]):
+        for x in R[i]:
+            s += x * x
+    tol = 1e-12 * math.sqrt(s)
+    for i in range(n):
+        if not abs(R[i, i]) > tol:
+            raise rank_error(f"recover_q: triangular factor is singular at column {i}")
+    A = join_rows(rels, tree, cap)
+    Q = np.zeros_like(A)
+    for j in range(n):
+        acc = A[:, j].copy()
+        for i in range(j):
+            acc = acc - Q[:, i] * R[i, j]
+        Q[:, j] = acc / R[j, j]
+    return A, Q
+
+
 def from_fgdb(db) -> Tuple[List[Relation], int, List[int]]:
     rels = [Relation(r.name, r.key_attrs, r.data_attrs, r.keys, r.data) for r in db.relations]
     return rels, db.root, list(db.parent)

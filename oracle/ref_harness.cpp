@@ -21,6 +21,10 @@
 //        random_acyclic_database (testbench.hpp:164), already reduced.
 //   ground_truth P Q N1 N2 SEED OUT.fgdb OUT_RFIXED.bin
 //        generate_ground_truth (testbench.hpp:51).
+//   q IN.fgdb IN.fgrs OUT.fgrq [--cap N]
+//        recover_q (postprocess.hpp:293) with the R stored in IN.fgrs, on the
+//        relations as read (not canonicalised): every streamed (a_row, q_row)
+//        pair, in for_each_join_row order (join.hpp:47).
 
 #include <chrono>
 #include <cstdio>
@@ -300,6 +304,42 @@ int cmd_ground_truth(int argc, char** argv) {
   return 0;
 }
 
+int cmd_q(int argc, char** argv) {
+  if (argc < 5) throw std::runtime_error("q IN.fgdb IN.fgrs OUT.fgrq [--cap N]");
+  Db db = read_db(argv[2]);
+  std::uint64_t cap = kDefaultJoinCap;
+  for (int i = 5; i + 1 < argc; i += 2)
+    if (std::string(argv[i]) == "--cap") cap = std::stoull(argv[i + 1]);
+  Reader rr(argv[3]);
+  char magic[8];
+  rr.arr(magic, 8);
+  if (std::memcmp(magic, "FGRS0001", 8) != 0) throw std::runtime_error("bad FGRS magic");
+  (void)rr.get<std::uint32_t>();
+  const auto n = rr.get<std::uint64_t>();
+  TriangularFactor f;
+  f.r = Matrix(n, n);
+  rr.arr(f.r.data(), n * n);
+  JoinTree tree = build_join_tree(db.rels, db.root, db.parent);
+  Layout layout = make_layout(db.rels, tree);
+  std::vector<double> a_rows, q_rows;
+  const std::uint64_t rows = recover_q(
+      db.rels, tree, layout, f,
+      [&](std::span<const double> a, std::span<const double> q) {
+        a_rows.insert(a_rows.end(), a.begin(), a.end());
+        q_rows.insert(q_rows.end(), q.begin(), q.end());
+      },
+      cap);
+  Writer w(argv[4]);
+  w.arr("FGRQ0001", 8);
+  w.put<std::uint64_t>(rows);
+  w.put<std::uint64_t>(n);
+  w.arr(a_rows.data(), a_rows.size());
+  w.arr(q_rows.data(), q_rows.size());
+  std::printf("ok rows=%llu n=%llu\n", static_cast<unsigned long long>(rows),
+              static_cast<unsigned long long>(n));
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -310,6 +350,7 @@ int main(int argc, char** argv) {
     if (mode == "materialized") return cmd_materialized(argc, argv);
     if (mode == "random") return cmd_random(argc, argv);
     if (mode == "ground_truth") return cmd_ground_truth(argc, argv);
+    if (mode == "q") return cmd_q(argc, argv);
     throw std::runtime_error("unknown mode " + mode);
   } catch (const integrity_error& e) {
     std::fprintf(stderr, "figaro_ref: integrity_error: %s\n", e.what());
@@ -317,6 +358,9 @@ int main(int argc, char** argv) {
   } catch (const size_error& e) {
     std::fprintf(stderr, "figaro_ref: size_error: %s\n", e.what());
     return 4;
+  } catch (const rank_error& e) {
+    std::fprintf(stderr, "figaro_ref: rank_error: %s\n", e.what());
+    return 5;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "figaro_ref: error: %s\n", e.what());
     return 2;

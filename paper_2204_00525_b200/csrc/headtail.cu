@@ -25,6 +25,8 @@
 // All results are run-to-run deterministic.
 #include <cuda_pipeline.h>
 
+#include <cub/block/block_scan.cuh>
+
 #include <type_traits>
 
 #include <string>
@@ -531,56 +533,54 @@ __global__ void k_unit_cont(HtDev a, int* __restrict__ cont, int* __restrict__ u
 }
 
 // Pre-pass: per unit, the partial sums of its last group if that group is
-// longer than kLight and continues into the next unit.  Row indices are
-// fetched 32 at a time; lanes sum column pairs with 16-byte loads when the
-// rows are 16-byte aligned.
+// longer than kLight and continues into the next unit.  The warp splits into
+// G row-groups of L lanes (L >= column packets of VEC doubles, as in the main
+// kernel); group grp sums rows q0+grp, q0+grp+G, ... and the G partial sums
+// are combined by a fixed xor-shuffle tree (deterministic).
 template <int VEC>
 __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
-                                 double* __restrict__ val) {
+                                 double* __restrict__ val, Geo geo) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool weighted = a.weights != nullptr;
   const int V = a.w + (weighted ? 1 : 0);
-  const int np = (a.w + VEC - 1) / VEC;
+  const int np = geo.np;
+  const int grp = lane / geo.L, cl = lane % geo.L;
   for (int64_t u = warp; u < a.n_units; u += nw) {
     const int64_t p0 = u * kUnit;
     const int64_t p1 = min(p0 + kUnit, a.n_rows);
     const int g = cont[u];
     if (g < 0) continue;
     const int64_t q0 = max((int64_t)a.begins[g], p0);
-    for (int pb = 0; pb < max(np, 1); pb += 32) {
-      const int pk = pb + lane;
+    for (int pb = 0; pb < max(np, 1); pb += geo.L) {
+      const int pk = pb + cl;
       double s[VEC];
 #pragma unroll
       for (int e = 0; e < VEC; ++e) s[e] = 0.0;
       double nacc = 0.0;
-      for (int64_t base = q0; base < p1; base += 32) {
-        const int cnt = (int)(p1 - base < 32 ? p1 - base : 32);
-        int64_t my_row = 0;
-        double my_w = 1.0;
-        if (lane < cnt) {
-          my_row = src_row(a, base + lane);
-          if (weighted) my_w = a.weights[my_row];
-        }
-#pragma unroll 8
-        for (int t = 0; t < cnt; ++t) {
-          const int64_t r = __shfl_sync(0xffffffffu, my_row, t);
-          const double v = weighted ? __shfl_sync(0xffffffffu, my_w, t) : 1.0;
-          if (pk < np) {
-            const double* src = a.data + r * a.ld + VEC * pk;
-            if (VEC == 2) {
-              const double2 x = *reinterpret_cast<const double2*>(src);
-              s[0] = weighted ? fma(v, x.x, s[0]) : s[0] + x.x;
-              s[VEC - 1] = weighted ? fma(v, x.y, s[VEC - 1]) : s[VEC - 1] + x.y;
-            } else {
-              s[0] = weighted ? fma(v, src[0], s[0]) : s[0] + src[0];
-            }
+#pragma unroll 4
+      for (int64_t p = q0 + grp; p < p1; p += geo.G) {
+        const int64_t r = src_row(a, p);
+        const double v = weighted ? a.weights[r] : 1.0;
+        if (pk < np) {
+          const double* src = a.data + r * a.ld + VEC * pk;
+          if (VEC == 2) {
+            const double2 x = *reinterpret_cast<const double2*>(src);
+            s[0] = weighted ? fma(v, x.x, s[0]) : s[0] + x.x;
+            s[VEC - 1] = weighted ? fma(v, x.y, s[VEC - 1]) : s[VEC - 1] + x.y;
+          } else {
+            s[0] = weighted ? fma(v, src[0], s[0]) : s[0] + src[0];
           }
-          nacc = fma(v, v, nacc);
         }
+        nacc = fma(v, v, nacc);
       }
-      if (pk < np)
+      for (int o = geo.L; o < 32; o <<= 1) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) s[e] += __shfl_xor_sync(0xffffffffu, s[e], o);
+        nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+      }
+      if (grp == 0 && pk < np)
 #pragma unroll
         for (int e = 0; e < VEC; ++e)
           if (VEC * pk + e < a.w) val[u * (int64_t)V + VEC * pk + e] = s[e];
@@ -595,7 +595,7 @@ __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
 //   k_chain_local: per block of kChainBlk units, per column, the in-block
 //                  inclusive run sums (written to carry[u+1]) and the block's
 //                  trailing run sum;
-//   k_chain_top:   sequential over blocks: the carry entering each block;
+//   k_chain_top:   segmented scan over blocks: the carry entering each block;
 //   k_chain_fix:   adds the entering carry to units whose chain started in an
 //                  earlier block.
 constexpr int kChainBlk = 128;
@@ -624,23 +624,49 @@ __global__ void k_chain_local(int64_t n_units, int V, const int* __restrict__ co
   }
 }
 
-__global__ void k_chain_top(int64_t n_blocks, int64_t n_units, int V,
-                            const int* __restrict__ cont,
-                            const double* __restrict__ tailsum,
-                            const int* __restrict__ starts_in,
-                            double* __restrict__ cin, const int* any) {
+// Segmented-sum pair: v is the running sum since the last reset (f = 1).
+struct SegPair {
+  double v;
+  int f;
+};
+struct SegOp {
+  __device__ __forceinline__ SegPair operator()(const SegPair& x, const SegPair& y) const {
+    return {y.f ? y.v : x.v + y.v, x.f | y.f};
+  }
+};
+constexpr int kTopThreads = 256, kTopItems = 4;
+
+// One CTA per column: exclusive segmented scan over the blocks' trailing
+// sums (reset where a chain starts inside the block), by cub::BlockScan in
+// chunks -- a fixed association, so the carries are deterministic.
+__global__ void __launch_bounds__(kTopThreads)
+    k_chain_top(int64_t n_blocks, int64_t n_units, int V, const int* __restrict__ cont,
+                const double* __restrict__ tailsum, const int* __restrict__ starts_in,
+                double* __restrict__ cin, const int* any) {
   if (!*any) return;
-  for (int col = threadIdx.x; col < V; col += blockDim.x) {
-    double c = 0.0;
-    for (int64_t b = 0; b < n_blocks; ++b) {
+  using Scan = cub::BlockScan<SegPair, kTopThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int col = blockIdx.x;
+  SegPair carry{0.0, 0};
+  for (int64_t base = 0; base < n_blocks; base += kTopThreads * kTopItems) {
+    SegPair it[kTopItems];
+#pragma unroll
+    for (int i = 0; i < kTopItems; ++i) {
+      const int64_t b = base + threadIdx.x * kTopItems + i;
+      it[i] = b < n_blocks ? SegPair{tailsum[b * V + col], starts_in[b]} : SegPair{0.0, 0};
+    }
+    SegPair agg;
+    Scan(tmp).ExclusiveScan(it, it, SegPair{0.0, 0}, SegOp(), agg);
+#pragma unroll
+    for (int i = 0; i < kTopItems; ++i) {
+      const int64_t b = base + threadIdx.x * kTopItems + i;
+      if (b >= n_blocks) continue;
       const int64_t u0 = b * kChainBlk;
       const bool cont_in = u0 > 0 && cont[u0] >= 0 && cont[u0 - 1] == cont[u0];
-      const double in = cont_in ? c : 0.0;
-      cin[b * V + col] = in;
-      // Carry leaving block b: its trailing run, plus what entered if the
-      // run reaches back to the block start.
-      c = starts_in[b] ? tailsum[b * V + col] : in + tailsum[b * V + col];
+      cin[b * V + col] = cont_in ? SegOp()(carry, it[i]).v : 0.0;
     }
+    carry = SegOp()(carry, agg);
+    __syncthreads();  // tmp is reused by the next chunk
   }
 }
 
@@ -698,24 +724,32 @@ __global__ void __launch_bounds__(256) k_join_rows(const __grid_constant__ JoinA
   }
 }
 
+constexpr int kJoinTile = 256;  // summary rows per k_join_elems tile
+
 __global__ void __launch_bounds__(256) k_join_elems(const __grid_constant__ JoinArgs a,
                                                     const double* __restrict__ fac) {
   const int nc = a.n_children;
-  const int64_t total = a.G * a.width;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = e / a.width;
-    const int j = (int)(e - k * a.width);
-    const double* f = fac + k * (nc + 1);
-    if (j < a.own_w) {
-      a.S[e] *= f[nc];
-      continue;
+  const unsigned width = (unsigned)a.width;
+  // Row tiles keep the element -> (row, column) split in 32-bit arithmetic.
+  for (int64_t k0 = blockIdx.x * (int64_t)kJoinTile; k0 < a.G;
+       k0 += (int64_t)gridDim.x * kJoinTile) {
+    const unsigned rows = (unsigned)(a.G - k0 < kJoinTile ? a.G - k0 : kJoinTile);
+    double* S = a.S + k0 * a.width;
+    for (unsigned le = threadIdx.x; le < rows * width; le += blockDim.x) {
+      const unsigned kk = le / width;
+      const int j = (int)(le - kk * width);
+      const int64_t k = k0 + kk;
+      const double* f = fac + k * (nc + 1);
+      if (j < a.own_w) {
+        S[le] *= f[nc];
+        continue;
+      }
+      int c = 0;
+      while (c + 1 < nc && j >= a.child_off[c + 1]) ++c;
+      const int idx = a.lidx[c][k];
+      if (idx < 0) continue;
+      S[le] = a.child_S[c][(int64_t)idx * a.child_w[c] + (j - a.child_off[c])] * f[c];
     }
-    int c = 0;
-    while (c + 1 < nc && j >= a.child_off[c + 1]) ++c;
-    const int idx = a.lidx[c][k];
-    if (idx < 0) continue;
-    a.S[e] = a.child_S[c][(int64_t)idx * a.child_w[c] + (j - a.child_off[c])] * f[c];
   }
 }
 
@@ -804,12 +838,18 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     FG_KERNEL_CHECK();
     const bool vec2 = in.w % 2 == 0 && in.ld % 2 == 0 &&
                       reinterpret_cast<uintptr_t>(in.data) % 16 == 0;
+    Geo tg{};
+    tg.vec = vec2 ? 2 : 1;
+    tg.np = in.w > 0 ? (in.w + tg.vec - 1) / tg.vec : 1;
+    tg.L = 1;
+    while (tg.L < tg.np && tg.L < 32) tg.L <<= 1;
+    tg.G = 32 / tg.L;
     if (vec2)
       k_unit_tail_sums<2><<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(
-          d, cont.get(), val.get());
+          d, cont.get(), val.get(), tg);
     else
       k_unit_tail_sums<1><<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(
-          d, cont.get(), val.get());
+          d, cont.get(), val.get(), tg);
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
     const int64_t nb = ceil_div(d.n_units, kChainBlk);
@@ -821,7 +861,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
                                                   any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
-    k_chain_top<<<1, ct, 0, ctx.stream>>>(nb, d.n_units, V, cont.get(), tailsum.get(),
+    k_chain_top<<<V, kTopThreads, 0, ctx.stream>>>(nb, d.n_units, V, cont.get(), tailsum.get(),
                                           starts.get(), cin.get(), any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
@@ -949,7 +989,7 @@ void launch_join(Context& ctx, const JoinArgs& a) {
   FG_KERNEL_CHECK();
   const int64_t total = a.G * a.width;
   if (total > 0) {
-    grid = std::min<int64_t>(ceil_div(total, threads), (int64_t)ctx.sm_count * 16);
+    grid = std::min<int64_t>(ceil_div(a.G, kJoinTile), (int64_t)ctx.sm_count * 16);
     k_join_elems<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a, fac.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();

@@ -169,4 +169,11 @@ struct Span {
 // R (n x n, row-major, device) of the stacked spans, sign-normalised.
 void tsqr(Context& ctx, const std::vector<Span>& spans, int n, double* R_out);
 
+// ---- join.cu ---------------------------------------------------------------
+// Join rows in for_each_join_row order; count only when A_out and Q_out are
+// null; Q = A R^-1 when Q_out is set (R host or device per `memory`).
+void join_rows(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
+               const int32_t* parent, int32_t memory, uint64_t cap, const double* R,
+               double* A_out, double* Q_out, int64_t* rows_out);
+
 }  // namespace fg

@@ -25,6 +25,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 
+#include "host_tree.hpp"
 #include "launchers.cuh"
 
 namespace fg {
@@ -84,177 +85,6 @@ struct Context::Saved {
 };
 
 namespace {
-
-// ---------------------------------------------------------------- host tree
-
-void build_tree(std::vector<std::unique_ptr<NodeState>>& nodes, int root,
-                const int32_t* parent, std::vector<int>& preorder) {
-  const int r = (int)nodes.size();
-  if (r == 0) fail(FG_E_TREE, "join tree: no relations");
-  if (root < 0 || root >= r) fail(FG_E_TREE, "join tree: bad root index");
-  for (int i = 0; i < r; ++i) {
-    const int p = parent[i];
-    nodes[i]->parent = p;
-    if (i == root) {
-      if (p != -1) fail(FG_E_TREE, "join tree: root cannot have a parent");
-      continue;
-    }
-    if (p < 0 || p >= r)
-      fail(FG_E_TREE, "join tree: bad parent index for node " + nodes[i]->name);
-    nodes[p]->children.push_back(i);
-    // parent_attrs: shared key attributes sorted by name (join_tree.hpp:37-45)
-    std::set<std::string> pk(nodes[p]->key_names.begin(),
-                             nodes[p]->key_names.end());
-    std::vector<std::string> shared;
-    for (const auto& k : nodes[i]->key_names)
-      if (pk.count(k)) shared.push_back(k);
-    std::sort(shared.begin(), shared.end());
-    nodes[i]->pattr_names = shared;
-  }
-  std::vector<int> stack{root};
-  std::vector<char> seen(r, 0);
-  // Pre-order, children in index order (join_tree.hpp:47-51).
-  std::function<void(int)> walk = [&](int n) {
-    if (seen[n]) fail(FG_E_TREE, "join tree: not a connected tree");
-    seen[n] = 1;
-    preorder.push_back(n);
-    for (int c : nodes[n]->children) walk(c);
-  };
-  walk(root);
-  if ((int)preorder.size() != r)
-    fail(FG_E_TREE, "join tree: not a connected tree");
-}
-
-// join_tree.hpp:104-180 (path property, every key attribute shared, data
-// attribute names disjoint from everything else) + canonicalize's schema
-// checks (relation.hpp:128-146).
-void validate(const std::vector<std::unique_ptr<NodeState>>& nodes) {
-  for (const auto& n : nodes) {
-    std::vector<std::string> names = n->key_names;
-    names.insert(names.end(), n->data_names.begin(), n->data_names.end());
-    std::sort(names.begin(), names.end());
-    auto dup = std::adjacent_find(names.begin(), names.end());
-    if (dup != names.end())
-      fail(FG_E_SCHEMA, "relation " + n->name + ": duplicate attribute '" +
-                            *dup + "'");
-    for (const auto& s : names)
-      if (s.empty())
-        fail(FG_E_SCHEMA, "relation " + n->name + ": empty attribute name");
-  }
-  const int r = (int)nodes.size();
-  if (r <= 1) return;
-  auto path_between = [&](int a, int b) {
-    std::vector<int> up_a, up_b;
-    for (int x = a; x != -1; x = nodes[x]->parent) up_a.push_back(x);
-    for (int x = b; x != -1; x = nodes[x]->parent) up_b.push_back(x);
-    std::set<int> anc(up_a.begin(), up_a.end());
-    int meet = -1;
-    for (int x : up_b)
-      if (anc.count(x)) { meet = x; break; }
-    std::vector<int> path;
-    for (int x : up_a) { path.push_back(x); if (x == meet) break; }
-    std::vector<int> down;
-    for (int x : up_b) { if (x == meet) break; down.push_back(x); }
-    path.insert(path.end(), down.rbegin(), down.rend());
-    return path;
-  };
-  std::map<std::string, std::vector<int>> attr_nodes;
-  for (int i = 0; i < r; ++i)
-    for (const auto& a : nodes[i]->key_names) attr_nodes[a].push_back(i);
-  for (const auto& [attr, ns] : attr_nodes) {
-    if (ns.size() < 2)
-      fail(FG_E_TREE, "key attribute '" + attr + "' of relation " +
-                          nodes[ns[0]]->name +
-                          " is not shared with any other relation");
-    for (size_t x = 0; x < ns.size(); ++x)
-      for (size_t y = x + 1; y < ns.size(); ++y)
-        for (int n : path_between(ns[x], ns[y])) {
-          const auto& ks = nodes[n]->key_names;
-          if (std::find(ks.begin(), ks.end(), attr) == ks.end())
-            fail(FG_E_TREE, "path property violated for attribute '" + attr +
-                                "': relation " + nodes[n]->name +
-                                " does not contain it");
-        }
-  }
-  std::map<std::string, int> data_owner;
-  for (int i = 0; i < r; ++i)
-    for (const auto& a : nodes[i]->data_names) {
-      auto [it, fresh] = data_owner.emplace(a, i);
-      if (!fresh)
-        fail(FG_E_SCHEMA, "data attribute '" + a + "' appears in both " +
-                              nodes[it->second]->name + " and " +
-                              nodes[i]->name);
-      if (attr_nodes.count(a))
-        fail(FG_E_SCHEMA, "attribute '" + a + "' is a data column of " +
-                              nodes[i]->name + " but a key column elsewhere");
-    }
-}
-
-struct Layout {
-  int64_t total = 0;
-  std::vector<int64_t> node_offset, node_width, sub_begin, sub_end;
-};
-
-Layout make_layout(const std::vector<std::unique_ptr<NodeState>>& nodes,
-                   const std::vector<int>& preorder, int root) {
-  Layout l;
-  const size_t r = nodes.size();
-  l.node_offset.resize(r);
-  l.node_width.resize(r);
-  l.sub_begin.resize(r);
-  l.sub_end.resize(r);
-  for (int n : preorder) {
-    l.node_offset[n] = l.total;
-    l.node_width[n] = nodes[n]->w;
-    l.total += nodes[n]->w;
-  }
-  std::function<int64_t(int)> fill = [&](int n) -> int64_t {
-    l.sub_begin[n] = l.node_offset[n];
-    int64_t end = l.node_offset[n] + l.node_width[n];
-    for (int c : nodes[n]->children) end = fill(c);
-    l.sub_end[n] = end;
-    return end;
-  };
-  fill(root);
-  return l;
-}
-
-// ---------------------------------------------------------------- encoding
-
-struct AttrCode {
-  long long min = 0;
-  int bits = 0;
-};
-
-int bitlen(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
-
-// Fields of `attrs` (attribute ids, in this order) packed MSB first, taking
-// values from source positions given by `src(attr)`.
-PackSpec make_spec(const std::vector<int>& attrs,
-                   const std::vector<AttrCode>& code,
-                   const std::function<int(int)>& src, int* total_bits,
-                   const std::string& what) {
-  PackSpec s{};
-  if (attrs.size() > (size_t)kMaxKeyCols)
-    fail(FG_E_UNSUPPORTED, what + ": more than 16 key attributes");
-  s.n = (int)attrs.size();
-  int total = 0;
-  for (int a : attrs) total += code[a].bits;
-  if (total > 64)
-    fail(FG_E_UNSUPPORTED, what + ": key tuple needs " + std::to_string(total) +
-                               " bits after range packing (> 64)");
-  int pos = total;
-  for (int f = 0; f < s.n; ++f) {
-    const int a = attrs[f];
-    pos -= code[a].bits;
-    s.shift[f] = pos;
-    s.bits[f] = code[a].bits;
-    s.min[f] = code[a].min;
-    s.col[f] = src(a);
-  }
-  if (total_bits) *total_bits = total;
-  return s;
-}
 
 // --------------------------------------------------------------- reduction
 
@@ -522,46 +352,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   tr.mark("setup+upload");
 
   // ---- attribute encodings (global, per attribute name)
-  std::map<std::string, int> attr_id;
-  for (auto& n : nodes)
-    for (const auto& k : n->key_names) {
-      auto it = attr_id.emplace(k, (int)attr_id.size()).first;
-      n->key_attr.push_back(it->second);
-    }
-  for (auto& n : nodes)
-    for (const auto& k : n->pattr_names) n->pattr.push_back(attr_id.at(k));
-  const int n_attr = (int)attr_id.size();
-  std::vector<AttrCode> code(n_attr);
-  if (n_attr) {
-    std::vector<long long> init_min(n_attr, LLONG_MAX), init_max(n_attr, LLONG_MIN);
-    DevArray<long long> dmin(n_attr, st), dmax(n_attr, st);
-    FG_CUDA(cudaMemcpyAsync(dmin.get(), init_min.data(), dmin.bytes(),
-                            cudaMemcpyHostToDevice, st));
-    FG_CUDA(cudaMemcpyAsync(dmax.get(), init_max.data(), dmax.bytes(),
-                            cudaMemcpyHostToDevice, st));
-    std::vector<DevArray<int>> col_attr;
-    for (auto& n : nodes) {
-      DevArray<int> ca(n->n_key, st);
-      if (n->n_key)
-        FG_CUDA(cudaMemcpyAsync(ca.get(), n->key_attr.data(), ca.bytes(),
-                                cudaMemcpyHostToDevice, st));
-      launch_key_minmax(ctx, n->keys, n->rows, n->n_key, ca.get(), dmin.get(),
-                        dmax.get());
-      col_attr.push_back(std::move(ca));
-    }
-    std::vector<long long> hmin(n_attr), hmax(n_attr);
-    FG_CUDA(cudaMemcpyAsync(hmin.data(), dmin.get(), dmin.bytes(),
-                            cudaMemcpyDeviceToHost, st));
-    FG_CUDA(cudaMemcpyAsync(hmax.data(), dmax.get(), dmax.bytes(),
-                            cudaMemcpyDeviceToHost, st));
-    FG_CUDA(cudaStreamSynchronize(st));
-    for (int a = 0; a < n_attr; ++a) {
-      if (hmin[a] > hmax[a]) { code[a] = {0, 0}; continue; }  // no rows
-      code[a].min = hmin[a];
-      code[a].bits = bitlen((uint64_t)hmax[a] - (uint64_t)hmin[a]);
-    }
-  }
-
+  std::vector<AttrCode> code = encode_attributes(ctx, nodes);
   tr.mark("encode (minmax sync)");
   // ---- semi-join reduction (reduce.hpp:47-74)
   if (!opt.assume_reduced) {
@@ -1285,6 +1076,36 @@ fg_status fg_tsqr(fg_ctx* c, int32_t n_blocks, const fg_block* blocks,
     }
     fg::tsqr(ctx, spans, n, R_out);
     FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+fg_status fg_join_size(fg_ctx* c, int32_t n_rel, const fg_relation* rels,
+                       int32_t root, const int32_t* parent, int32_t memory,
+                       uint64_t cap, int64_t* rows) {
+  return fg::guard(c, [&] {
+    fg::join_rows(*reinterpret_cast<Context*>(c), n_rel, rels, root, parent, memory,
+                  cap, nullptr, nullptr, nullptr, rows);
+  });
+}
+
+fg_status fg_materialize_join(fg_ctx* c, int32_t n_rel, const fg_relation* rels,
+                              int32_t root, const int32_t* parent, int32_t memory,
+                              uint64_t cap, double* A_out, int64_t* rows) {
+  return fg::guard(c, [&] {
+    if (!A_out) fail(FG_E_ARG, "A_out is null");
+    fg::join_rows(*reinterpret_cast<Context*>(c), n_rel, rels, root, parent, memory,
+                  cap, nullptr, A_out, nullptr, rows);
+  });
+}
+
+fg_status fg_recover_q(fg_ctx* c, int32_t n_rel, const fg_relation* rels,
+                       int32_t root, const int32_t* parent, int32_t memory,
+                       uint64_t cap, const double* R, double* A_out, double* Q_out,
+                       int64_t* rows) {
+  return fg::guard(c, [&] {
+    if (!R) fail(FG_E_ARG, "recover_q: R is null");
+    fg::join_rows(*reinterpret_cast<Context*>(c), n_rel, rels, root, parent, memory,
+                  cap, R, A_out, Q_out, rows);
   });
 }
 

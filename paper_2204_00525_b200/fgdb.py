@@ -220,3 +220,16 @@ def read_fgrm(path: str) -> np.ndarray:
     rd.o = 8
     n = rd.u64()
     return rd.arr("<f8", n * n).reshape(n, n)
+
+
+def read_fgrq(path: str):
+    """recover_q output of the reference harness: (A rows, Q rows)."""
+    with open(path, "rb") as f:
+        rd = _Rd(f.read())
+    assert bytes(rd.b[:8]) == b"FGRQ0001", "bad FGRQ magic"
+    rd.o = 8
+    rows = rd.u64()
+    n = rd.u64()
+    A = rd.arr("<f8", rows * n).reshape(rows, n)
+    Q = rd.arr("<f8", rows * n).reshape(rows, n)
+    return A, Q

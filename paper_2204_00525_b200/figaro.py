@@ -69,7 +69,7 @@ class cuda_error(error):
 _ERR = {L.FG_E_ARG: error, L.FG_E_SCHEMA: schema_error, L.FG_E_TREE: tree_error,
         L.FG_E_INTEGRITY: integrity_error, L.FG_E_SIZE: size_error,
         L.FG_E_EMPTY_JOIN: empty_join_error, L.FG_E_UNSUPPORTED: unsupported_error,
-        L.FG_E_CUDA: cuda_error}
+        L.FG_E_CUDA: cuda_error, L.FG_E_RANK: rank_error}
 
 
 # ---------------------------------------------------------------- context
@@ -329,19 +329,11 @@ def _cstrs(names):
     return arr
 
 
-def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
-                 opts: PipelineOptions = PipelineOptions(), keep_r0: bool = False,
-                 device: int = 0, fetch_counts: bool = True,
-                 fuse: bool = True) -> PipelineResult:
-    """driver.hpp:47-85 on the GPU.  Host (numpy) relations are copied to the
-    device inside the call; torch CUDA relations are used in place and R is
-    returned as a CUDA tensor."""
-    ctx = get_context(device)
-    lib = ctx.lib
-    rels = list(relations)
+def _marshal(rels, what):
+    """fg_relation array for the C ABI (+ objects to keep alive, device flag)."""
     on_dev = [r.on_device for r in rels]
     if any(on_dev) and not all(on_dev):
-        raise error("run_pipeline: mix of host and device relations")
+        raise error(f"{what}: mix of host and device relations")
     device_mem = bool(rels) and all(on_dev)
     keep = []
     arr = (L.fg_relation * len(rels))()
@@ -354,6 +346,20 @@ def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
             kp, dp = r.keys.ctypes.data, r.data.ctypes.data
         arr[i] = L.fg_relation(r.name.encode(), len(r.key_attrs), ka, len(r.data_attrs), da,
                                r.row_count(), kp, dp)
+    return arr, keep, device_mem
+
+
+def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
+                 opts: PipelineOptions = PipelineOptions(), keep_r0: bool = False,
+                 device: int = 0, fetch_counts: bool = True,
+                 fuse: bool = True) -> PipelineResult:
+    """driver.hpp:47-85 on the GPU.  Host (numpy) relations are copied to the
+    device inside the call; torch CUDA relations are used in place and R is
+    returned as a CUDA tensor."""
+    ctx = get_context(device)
+    lib = ctx.lib
+    rels = list(relations)
+    arr, keep, device_mem = _marshal(rels, "run_pipeline")
     parent = (C.c_int32 * len(rels))(*tree.parent)
     o = L.fg_options()
     lib.fg_options_default(C.byref(o))
@@ -445,6 +451,99 @@ def fetch_r0(ctx: Context) -> List[OutSpan]:
 
 # ---------------------------------------------------------------- phase API
 # Thin wrappers over the phase-level kernels; arguments are torch CUDA tensors.
+
+
+# ------------------------------------------------ join rows and Q = A R^-1
+
+DEFAULT_JOIN_CAP = 1_000_000  # kDefaultJoinCap (join.hpp:25)
+
+
+def join_size(relations: Sequence[Relation], tree: JoinTree, cap: int = DEFAULT_JOIN_CAP,
+              device: int = 0) -> int:
+    """for_each_join_row with an empty sink (join.hpp:47-92): the number of
+    join rows; more than `cap` raises size_error."""
+    ctx = get_context(device)
+    rels = list(relations)
+    arr, keep, device_mem = _marshal(rels, "join_size")
+    parent = (C.c_int32 * len(rels))(*tree.parent)
+    rows = C.c_int64()
+    ctx.check(ctx.lib.fg_join_size(ctx.h, len(rels), arr, tree.root, parent,
+                                   L.FG_MEM_DEVICE if device_mem else L.FG_MEM_HOST,
+                                   C.c_uint64(cap), C.byref(rows)))
+    del keep
+    return rows.value
+
+
+def _out(rows, n, device_mem, like):
+    if device_mem:
+        import torch
+        t = torch.empty((rows, n), dtype=torch.float64, device=like.device)
+        return t, t.data_ptr()
+    a = np.zeros((rows, n))
+    return a, a.ctypes.data
+
+
+def materialize_join(relations: Sequence[Relation], tree: JoinTree,
+                     cap: int = DEFAULT_JOIN_CAP, device: int = 0):
+    """materialize_join (join.hpp:96-112): the dense join, rows in
+    for_each_join_row order, columns in the pre-order layout."""
+    ctx = get_context(device)
+    rels = list(relations)
+    n = make_layout(rels, tree).total
+    rows = join_size(rels, tree, cap, device)
+    arr, keep, device_mem = _marshal(rels, "materialize_join")
+    A, ap = _out(rows, n, device_mem, rels[0].data if rels else None)
+    if rows and n:
+        parent = (C.c_int32 * len(rels))(*tree.parent)
+        got = C.c_int64()
+        ctx.check(ctx.lib.fg_materialize_join(
+            ctx.h, len(rels), arr, tree.root, parent,
+            L.FG_MEM_DEVICE if device_mem else L.FG_MEM_HOST, C.c_uint64(cap),
+            C.c_void_p(ap), C.byref(got)))
+    del keep
+    return A
+
+
+def recover_q(relations: Sequence[Relation], tree: JoinTree, R, cap: int = DEFAULT_JOIN_CAP,
+              with_rows: bool = True, device: int = 0):
+    """recover_q (postprocess.hpp:293-321) on the GPU: returns (A, Q) -- the
+    join rows handed to the reference's sink and Q = A R^-1 -- (A is None
+    with with_rows=False).  R: the n x n factor (numpy, or a CUDA tensor when
+    the relations are on the device).  Singular R raises rank_error."""
+    ctx = get_context(device)
+    rels = list(relations)
+    n = make_layout(rels, tree).total
+    arr, keep, device_mem = _marshal(rels, "recover_q")
+    if device_mem:
+        Rc = R.contiguous()
+        rp = Rc.data_ptr()
+    else:
+        Rc = np.ascontiguousarray(np.asarray(R, dtype=np.float64))
+        rp = Rc.ctypes.data
+    if tuple(Rc.shape) != (n, n):
+        raise error("recover_q: factor size does not match column layout")
+    parent = (C.c_int32 * len(rels))(*tree.parent)
+    mem = L.FG_MEM_DEVICE if device_mem else L.FG_MEM_HOST
+    rows = C.c_int64()
+    # Rank check, then the cap check and the row count (no outputs yet).
+    ctx.check(ctx.lib.fg_recover_q(ctx.h, len(rels), arr, tree.root, parent, mem,
+                                   C.c_uint64(cap), C.c_void_p(rp), None, None,
+                                   C.byref(rows)))
+    like = rels[0].data if rels else None
+    if rows.value == 0 or n == 0:
+        Q, _ = _out(rows.value, n, device_mem, like)
+        A = _out(rows.value, n, device_mem, like)[0] if with_rows else None
+        del keep, Rc
+        return A, Q
+    Q, qp = _out(rows.value, n, device_mem, like)
+    A, ap = _out(rows.value, n, device_mem, like) if with_rows else (None, None)
+    got = C.c_int64()
+    ctx.check(ctx.lib.fg_recover_q(ctx.h, len(rels), arr, tree.root, parent, mem,
+                                   C.c_uint64(cap), C.c_void_p(rp),
+                                   C.c_void_p(ap) if ap else None, C.c_void_p(qp),
+                                   C.byref(got)))
+    del keep, Rc
+    return A, Q
 
 
 def group_keys(keys, bits: int, device: int = 0):

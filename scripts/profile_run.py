@@ -12,6 +12,6 @@ rels = [Relation(r.name, r.key_attrs, r.data_attrs, torch.from_numpy(r.keys).cud
                  torch.from_numpy(r.data).cuda()) for r in db.relations]
 tree = build_join_tree(rels, db.root, db.parent)
 for _ in range(reps):
-    res = run_pipeline(rels, tree, PipelineOptions(assume_reduced=True), fetch_counts=False)
+    res = run_pipeline(rels, tree, PipelineOptions(assume_reduced=True), fetch_counts=False, fuse=os.environ.get("FUSE", "1") == "1")
 torch.cuda.synchronize()
 print("ok", cfg, scale, res.seconds_total)

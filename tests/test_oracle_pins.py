@@ -217,3 +217,75 @@ def test_c1_golden_checksum_and_oracle():
     ref = fgdb.read_fgrs(golden("c1_seed7.fgrs"))
     assert [n.rows_per_key.tolist() for n in ref.nodes] == [[10] * 1000] * 2
     assert [n.phi_circ.tolist() for n in ref.nodes] == [[10] * 1000] * 2
+
+
+# ---------------------------------------------------------------- join rows / Q
+
+
+def _mk(name, ka, da, rows):
+    keys = np.array([r[0] for r in rows], dtype=np.int64).reshape(len(rows), len(ka))
+    data = np.array([r[1] for r in rows], dtype=np.float64).reshape(len(rows), len(da))
+    return fo.Relation(name, ka, da, keys, data)
+
+
+def test_materialize_join_pins():
+    # test_relational.cpp:189-235
+    s = _mk("S", [], ["y1"], [([], [1.0]), ([], [2.0]), ([], [3.0])])
+    t = _mk("T", [], ["y2"], [([], [4.0]), ([], [5.0])])
+    a = fo.join_rows([s, t], fo.build_join_tree([s, t], 0, [-1, 0]))
+    assert a.shape == (6, 2)
+    np.testing.assert_array_equal(a[:, 0], [1, 1, 2, 2, 3, 3])  # depth-first order
+    s = _mk("S", ["X"], ["y", "z"], [([1], [1.0, 2.0]), ([2], [3.0, 4.0])])
+    a = fo.join_rows([s], fo.build_join_tree([s], 0, [-1]))
+    assert a.shape == (2, 2) and a[0, 0] == 1.0 and a[1, 1] == 4.0
+    s = _mk("S", ["X"], ["y"], [([1], [1.0]), ([1], [2.0])])
+    t = _mk("T", ["X"], ["z"], [([1], [3.0]), ([1], [4.0]), ([1], [5.0])])
+    assert fo.join_rows([s, t], fo.build_join_tree([s, t], 0, [-1, 0])).shape[0] == 6
+    s = _mk("S", [], ["y"], [([], [1.0]), ([], [2.0])])
+    t = _mk("T", [], ["z"], [([], [3.0]), ([], [4.0])])
+    with pytest.raises(fo.size_error):
+        fo.join_rows([s, t], fo.build_join_tree([s, t], 0, [-1, 0]), cap=3)
+
+
+def test_recover_q_pins():
+    # test_postprocess.cpp:185-247
+    s = _mk("S", [], ["y"], [([], [2.0])])
+    a, q = fo.recover_q([s], fo.build_join_tree([s], 0, [-1]), np.array([[2.0]]))
+    assert q.shape == (1, 1) and q[0, 0] == pytest.approx(1.0)
+    s = _mk("S", [], ["y1"], [([], [1.0]), ([], [2.0])])
+    t = _mk("T", [], ["y2"], [([], [1.0]), ([], [3.0])])
+    rels = [s, t]
+    tree = fo.build_join_tree(rels, 0, [-1, 0])
+    R = fo.run_pipeline(rels, 0, [-1, 0]).R
+    a, q = fo.recover_q(rels, tree, R)
+    assert q.shape[0] == 4
+    np.testing.assert_allclose(q.T @ q, np.eye(2), atol=1e-10)
+    assert rel_fro(q @ R, a) <= 1e-10
+    s = _mk("S", [], ["y", "z"], [([], [1.0, 1.0])])
+    with pytest.raises(fo.rank_error):
+        fo.recover_q([s], fo.build_join_tree([s], 0, [-1]), np.array([[1.0, 1.0], [0.0, 0.0]]))
+
+
+@pytest.mark.parametrize("stem", [s for s in golden_stems("hand_") + golden_stems("rnd_")
+                                  if __import__("os").path.exists(golden(s + ".fgrq"))])
+def test_oracle_recover_q_matches_reference(stem):
+    """The restated join order and forward substitution reproduce the
+    reference's streamed (a_row, q_row) pairs bit for bit."""
+    db = fgdb.read_fgdb(golden(stem + ".fgdb"))
+    R = fgdb.read_fgrs(golden(stem + ".fgrs")).R
+    A_ref, Q_ref = fgdb.read_fgrq(golden(stem + ".fgrq"))
+    rels, root, parent = fo.from_fgdb(db)
+    A, Q = fo.recover_q(rels, fo.build_join_tree(rels, root, parent), R, cap=5000)
+    np.testing.assert_array_equal(A, A_ref)
+    np.testing.assert_array_equal(Q, Q_ref)
+
+
+@pytest.mark.parametrize("stem,err", [("rnd_15", "rank"), ("rnd_19", "rank"),
+                                      ("rnd_10", "size"), ("rnd_4", "size")])
+def test_oracle_recover_q_errors(stem, err):
+    """The reference raised rank_error / size_error (cap 5000) on these."""
+    db = fgdb.read_fgdb(golden(stem + ".fgdb"))
+    R = fgdb.read_fgrs(golden(stem + ".fgrs")).R
+    rels, root, parent = fo.from_fgdb(db)
+    with pytest.raises(fo.rank_error if err == "rank" else fo.size_error):
+        fo.recover_q(rels, fo.build_join_tree(rels, root, parent), R, cap=5000)
