@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <map>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <variant>
@@ -58,9 +59,17 @@ struct DefaultErrors {
   }
 };
 
-template <class Rel, class Tree, class Errors = DefaultErrors>
-Result run_pipeline(Device& dev, const std::vector<Rel>& rels, const Tree& tree,
-                    bool assume_reduced = false) {
+// Flat C-ABI description of reference relations (keys encoded as int64).
+struct Marshalled {
+  std::vector<std::vector<int64_t>> keys;
+  std::vector<std::vector<const char*>> kn, dn;
+  std::vector<fg_relation> desc;
+  std::vector<int32_t> parent;
+  std::size_t n = 0;  // total data columns
+};
+
+template <class Rel, class Tree>
+void marshal(const std::vector<Rel>& rels, const Tree& tree, Marshalled& m) {
   const std::size_t r = rels.size();
   // Per attribute: integer keys pass through; string keys get ranks.
   std::map<std::string, std::vector<std::string>> strings;
@@ -73,38 +82,50 @@ Result run_pipeline(Device& dev, const std::vector<Rel>& rels, const Tree& tree,
     std::sort(v.begin(), v.end());
     v.erase(std::unique(v.begin(), v.end()), v.end());
   }
-  std::vector<std::vector<int64_t>> keys(r);
-  std::vector<std::vector<const char*>> kn(r), dn(r);
-  std::vector<fg_relation> desc(r);
-  std::vector<int32_t> parent(r);
+  m.keys.assign(r, {});
+  m.kn.assign(r, {});
+  m.dn.assign(r, {});
+  m.desc.assign(r, fg_relation{});
+  m.parent.assign(r, -1);
   for (std::size_t i = 0; i < r; ++i) {
     const auto& rel = rels[i];
     const std::size_t nk = rel.key_attrs.size();
-    keys[i].resize(rel.keys.size() * nk);
+    auto& keys = m.keys[i];
+    keys.resize(rel.keys.size() * nk);
     for (std::size_t row = 0; row < rel.keys.size(); ++row)
       for (std::size_t c = 0; c < nk; ++c) {
         const auto& kv = rel.keys[row][c];
         if (std::holds_alternative<std::string>(kv)) {
           const auto& v = strings[rel.key_attrs[c]];
-          keys[i][row * nk + c] =
+          keys[row * nk + c] =
               std::lower_bound(v.begin(), v.end(), std::get<std::string>(kv)) - v.begin();
         } else {
-          keys[i][row * nk + c] = std::get<int64_t>(kv);
+          keys[row * nk + c] = std::get<int64_t>(kv);
         }
       }
-    for (const auto& a : rel.key_attrs) kn[i].push_back(a.c_str());
-    for (const auto& a : rel.data_attrs) dn[i].push_back(a.c_str());
-    desc[i] = fg_relation{rel.name.c_str(), (int32_t)nk, kn[i].data(),
-                          (int32_t)rel.data.cols(), dn[i].data(),
-                          (int64_t)rel.keys.size(), keys[i].data(), rel.data.data()};
-    parent[i] = tree.nodes[i].parent;
+    for (const auto& a : rel.key_attrs) m.kn[i].push_back(a.c_str());
+    for (const auto& a : rel.data_attrs) m.dn[i].push_back(a.c_str());
+    m.desc[i] = fg_relation{rel.name.c_str(), (int32_t)nk, m.kn[i].data(),
+                            (int32_t)rel.data.cols(), m.dn[i].data(),
+                            (int64_t)rel.keys.size(), keys.data(), rel.data.data()};
+    m.parent[i] = tree.nodes[i].parent;
+    m.n += rel.data.cols();
   }
+}
+
+template <class Rel, class Tree, class Errors = DefaultErrors>
+Result run_pipeline(Device& dev, const std::vector<Rel>& rels, const Tree& tree,
+                    bool assume_reduced = false) {
+  const std::size_t r = rels.size();
+  Marshalled m;
+  marshal(rels, tree, m);
+  auto& desc = m.desc;
+  auto& parent = m.parent;
   fg_options o;
   fg_options_default(&o);
   o.assume_reduced = assume_reduced ? 1 : 0;
   o.memory = FG_MEM_HOST;
-  std::size_t n = 0;
-  for (const auto& rel : rels) n += rel.data.cols();
+  const std::size_t n = m.n;
   Result res;
   res.n = n;
   res.r.assign(n * n, 0.0);
@@ -119,6 +140,35 @@ Result run_pipeline(Device& dev, const std::vector<Rel>& rels, const Tree& tree,
   res.seconds_postprocess = out.seconds_postprocess;
   res.seconds_total = out.seconds_total;
   return res;
+}
+
+// recover_q (postprocess.hpp:293-321) on the device: streams every join row
+// (for_each_join_row order, join.hpp:47-92) and its Q = A R^-1 row to
+// sink(a_row, q_row); `r` is the n x n factor, row-major.  Returns the row
+// count.  Singular R -> FG_E_RANK, more than `cap` rows -> FG_E_SIZE, both
+// before the sink sees a row.
+template <class Rel, class Tree, class Errors = DefaultErrors, class Sink>
+std::uint64_t recover_q(Device& dev, const std::vector<Rel>& rels, const Tree& tree,
+                        const std::vector<double>& r, Sink&& sink,
+                        std::uint64_t cap = 1'000'000) {
+  Marshalled m;
+  marshal(rels, tree, m);
+  if (r.size() != m.n * m.n) Errors::raise(FG_E_ARG, "recover_q: factor size does not match column layout");
+  int64_t rows = 0;
+  fg_status st = fg_recover_q(dev.ctx, (int32_t)rels.size(), m.desc.data(), tree.root,
+                              m.parent.data(), FG_MEM_HOST, cap, r.data(), nullptr,
+                              nullptr, &rows);
+  if (st != FG_OK) Errors::raise(st, fg_last_error(dev.ctx));
+  std::vector<double> a((std::size_t)rows * m.n), q((std::size_t)rows * m.n);
+  if (rows && m.n) {
+    st = fg_recover_q(dev.ctx, (int32_t)rels.size(), m.desc.data(), tree.root,
+                      m.parent.data(), FG_MEM_HOST, cap, r.data(), a.data(), q.data(), &rows);
+    if (st != FG_OK) Errors::raise(st, fg_last_error(dev.ctx));
+  }
+  for (int64_t i = 0; i < rows; ++i)
+    sink(std::span<const double>(a.data() + i * m.n, m.n),
+         std::span<const double>(q.data() + i * m.n, m.n));
+  return (std::uint64_t)rows;
 }
 
 }  // namespace figaro::gpu

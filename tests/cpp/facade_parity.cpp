@@ -7,6 +7,7 @@
 #include <cstdio>
 
 #include "figaro/driver.hpp"
+#include "figaro/join.hpp"
 #include "figaro/testbench.hpp"
 #include "figaro_gpu.hpp"
 
@@ -20,6 +21,7 @@ struct RefErrors {
       case FG_E_TREE: throw figaro::tree_error(m);
       case FG_E_SCHEMA: throw figaro::schema_error(m);
       case FG_E_EMPTY_JOIN: throw figaro::empty_join_error(m);
+      case FG_E_RANK: throw figaro::rank_error(m);
       default: throw figaro::error(m);
     }
   }
@@ -66,6 +68,39 @@ int main() {
     for (std::size_t i = 0; i < ref.factor.r.rows() && full; ++i)
       full = std::abs(ref.factor.r(i, i)) > 1e-8 * std::abs(ref.factor.r(0, 0));
     const double d = rel_dist(got.r, ref.factor.r, !full);
+    // recover_q with the reference's R: identical (a_row, q_row) streams.
+    {
+      const figaro::Layout layout = figaro::make_layout(db.relations, db.tree);
+      std::vector<double> ra, rq, ga, gq;
+      bool ref_rank = false, gpu_rank = false;
+      try {
+        figaro::recover_q(db.relations, db.tree, layout, ref.factor,
+                          [&](std::span<const double> a, std::span<const double> q) {
+                            ra.insert(ra.end(), a.begin(), a.end());
+                            rq.insert(rq.end(), q.begin(), q.end());
+                          });
+      } catch (const figaro::rank_error&) {
+        ref_rank = true;
+      }
+      const auto& R = ref.factor.r;
+      std::vector<double> rv(R.data(), R.data() + R.rows() * R.cols());
+      try {
+        figaro::gpu::recover_q<figaro::Relation, figaro::JoinTree, RefErrors>(
+            dev, db.relations, db.tree, rv,
+            [&](std::span<const double> a, std::span<const double> q) {
+              ga.insert(ga.end(), a.begin(), a.end());
+              gq.insert(gq.end(), q.begin(), q.end());
+            });
+      } catch (const figaro::rank_error&) {
+        gpu_rank = true;
+      }
+      if (ref_rank != gpu_rank || ra != ga || rq != gq) {
+        ++bad;
+        std::printf("seed %llu: recover_q differs (rank %d/%d, rows %zu/%zu)\n",
+                    (unsigned long long)seed, (int)ref_rank, (int)gpu_rank, ra.size(),
+                    ga.size());
+      }
+    }
     worst = std::max(worst, d);
     if (d > 1e-10 || got.r0_rows != ref.r0_rows || got.input_rows != ref.input_rows) {
       ++bad;
