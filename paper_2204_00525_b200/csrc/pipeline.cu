@@ -562,7 +562,11 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     if (!is_leaf) n.S.zero();
     n.scale.alloc(G, st);
     const int64_t n_tails = n.rows - G;
-    const bool fuse = opt.fuse && !opt.keep_r0 && fused_width(n.w) > 0 && n_tails > 0;
+    // The fused kernel absorbs a zero row per group start; when groups are
+    // short (tails < 70% of the rows) writing the tails densely and factoring
+    // only them is cheaper (measured on C3's F: 9.1 ms fused vs 6.7 ms).
+    const bool fuse = opt.fuse && !opt.keep_r0 && fused_width(n.w) > 0 && n_tails > 0 &&
+                      n_tails * 10 >= n.rows * 7;
     if (n.w > 0 && n_tails > 0 && !fuse) n.tails.alloc(n_tails * n.w, st);
     HeadTailArgs a;
     a.data = n.data;

@@ -42,6 +42,12 @@ struct SegDev {
   int64_t row0;  // first row of this segment in the concatenated row space
 };
 
+}  // namespace
+}  // namespace fg
+#include "tsqr_blk.cuh"
+namespace fg {
+namespace {
+
 template <int W_, int TC_, int TR_, int RPT_>
 struct Cfg {
   static constexpr int W = W_;
@@ -315,6 +321,10 @@ using W20 = WCfg<20, 5, 8, 1>;
 using W24 = WCfg<24, 3, 8, 2>;
 using W32c = WCfg<32, 4, 8, 2>;
 using C16 = Cfg<16, 8, 16, 16>;
+using B32 = BCfg<32, 128>;
+using B32s = BCfg<32, 64>;
+using B64 = BCfg<64, 128>;
+using B64s = BCfg<64, 64>;
 using C32 = Cfg<32, 16, 16, 8>;
 
 // Kernel variant per width (FG_TSQR_W16 / FG_TSQR_W32 = warp | warpb |
@@ -324,9 +334,9 @@ int variant(int W) {
                          : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128" : "FG_TSQR_X");
   if (!e) return W == 16 ? 2 : W == 32 ? 3 : 0;  // measured best (tsqr_sweep.py)
   const std::string v = e;
-  if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : 0;
+  if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : v == "blk" ? 3 : v == "blk64" ? 4 : 0;
   return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : v == "warpd" ? 4
-         : v == "warpe" ? 5 : v == "warpf" ? 6 : v == "warpg" ? 7 : 0;
+         : v == "warpe" ? 5 : v == "warpf" ? 6 : v == "warpg" ? 7 : v == "blk" ? 8 : v == "blk64" ? 9 : 0;
 }
 
 int bucket(int w) {
@@ -357,6 +367,10 @@ Plan plan_cta(Context& ctx) {
   return {C::B, 1, resident(ctx, k_tsqr<C>, C::NT, C::smem_bytes)};
 }
 template <class C>
+Plan plan_blk(Context& ctx) {
+  return {C::B, 1, resident(ctx, k_tsqr_blk<C, SegDev>, C::NT, C::smem_bytes)};
+}
+template <class C>
 Plan plan_warp(Context& ctx) {
   return {C::B, C::WARPS, resident(ctx, k_tsqr_warp<C>, C::NT, C::smem_bytes)};
 }
@@ -376,6 +390,7 @@ Plan plan_for(Context& ctx, int W) {
     case 32: {
       const int v = variant(32);
       return v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
+                    : v == 8 ? plan_blk<B32>(ctx) : v == 9 ? plan_blk<B32s>(ctx)
                     : plan_warp<W32>(ctx);
     }
     case 12: return plan_warp<W12>(ctx);
@@ -383,7 +398,9 @@ Plan plan_for(Context& ctx, int W) {
     case 24: return plan_warp<W24>(ctx);
     case 64: {
       const int v = variant(64);
-      return v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx) : plan_cta<C64>(ctx);
+      return v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
+             : v == 3 ? plan_blk<B64>(ctx) : v == 4 ? plan_blk<B64s>(ctx)
+             : plan_cta<C64>(ctx);
     }
     default: {
       const int v = variant(128);
@@ -414,6 +431,8 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       const int v = variant(32);
       if (v == 2) k_tsqr_warp<W32c><<<grid, W32c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 3) k_tsqr<C32><<<grid, C32::NT, C32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 8) k_tsqr_blk<B32, SegDev><<<grid, B32::NT, B32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 9) k_tsqr_blk<B32s, SegDev><<<grid, B32s::NT, B32s::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else k_tsqr_warp<W32><<<grid, W32::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       break;
     }
@@ -424,6 +443,8 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       const int v = variant(64);
       if (v == 1) k_tsqr<C64a><<<grid, C64a::NT, C64a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 2) k_tsqr<C64b><<<grid, C64b::NT, C64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 3) k_tsqr_blk<B64, SegDev><<<grid, B64::NT, B64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 4) k_tsqr_blk<B64s, SegDev><<<grid, B64s::NT, B64s::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       break;
     }

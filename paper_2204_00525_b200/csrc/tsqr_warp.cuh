@@ -93,11 +93,11 @@ __device__ __forceinline__ double wgroup_sum(double x) {
 
 // One column step k of absorb_tile; QB (the column block) is compile-time,
 // the position inside the block may be a run-time value.
-template <class C, int QB>
+template <class C, int QB, bool REC = false>
 __device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
                                             double (&Racc)[C::RR][C::CPT],
                                             int r, int c, const int (&cols)[C::CPT],
-                                            int within) {
+                                            int within, double* rec = nullptr) {
   const int k = QB * C::TC + within;
   const int ck = (QB & 1) ? C::TC - 1 - within : within;
   const int rk = k % C::TR;   // lane row holding accumulator row k
@@ -123,6 +123,14 @@ __device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
   };
   const double alpha = __shfl_sync(0xffffffffu, racc(QB), rk + ck * C::TR);
   const Reflector h = make_reflector(alpha, sig);
+  if constexpr (REC) {
+    // Reflector k for the caller's block update: {u0, t1, t2}.
+    if ((threadIdx.x & 31) == 0) {
+      rec[3 * k] = h.u0;
+      rec[3 * k + 1] = h.t1;
+      rec[3 * k + 2] = h.t2;
+    }
+  }
 #pragma unroll
   for (int q = QB; q < C::CPT; ++q) {
     const bool act = cols[q] > k;
@@ -150,21 +158,22 @@ __device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
   }
 }
 
-template <class C, int QB>
+template <class C, int QB, bool REC = false>
 __device__ __forceinline__ void absorb_blocks(double (&X)[C::RPT][C::CPT],
                                               double (&Racc)[C::RR][C::CPT],
-                                              int r, int c, const int (&cols)[C::CPT]) {
+                                              int r, int c, const int (&cols)[C::CPT],
+                                              double* rec = nullptr) {
   if constexpr (QB < C::CPT) {
     if constexpr (C::ROLL) {
 #pragma unroll 1
       for (int within = 0; within < C::TC; ++within)
-        absorb_step<C, QB>(X, Racc, r, c, cols, within);
+        absorb_step<C, QB, REC>(X, Racc, r, c, cols, within, rec);
     } else {
 #pragma unroll
       for (int within = 0; within < C::TC; ++within)
-        absorb_step<C, QB>(X, Racc, r, c, cols, within);
+        absorb_step<C, QB, REC>(X, Racc, r, c, cols, within, rec);
     }
-    absorb_blocks<C, QB + 1>(X, Racc, r, c, cols);
+    absorb_blocks<C, QB + 1, REC>(X, Racc, r, c, cols, rec);
   }
 }
 
@@ -176,6 +185,15 @@ __device__ __forceinline__ void absorb_tile(double (&X)[C::RPT][C::CPT],
                                             double (&Racc)[C::RR][C::CPT],
                                             int r, int c, const int (&cols)[C::CPT]) {
   absorb_blocks<C, 0>(X, Racc, r, c, cols);
+}
+
+// Same, recording every reflector {u0, t1, t2} in rec[3k..3k+2] (lane 0).
+template <class C>
+__device__ __forceinline__ void absorb_tile_rec(double (&X)[C::RPT][C::CPT],
+                                                double (&Racc)[C::RR][C::CPT],
+                                                int r, int c, const int (&cols)[C::CPT],
+                                                double* rec) {
+  absorb_blocks<C, 0, true>(X, Racc, r, c, cols, rec);
 }
 
 }  // namespace fg
