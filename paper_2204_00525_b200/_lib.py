@@ -10,7 +10,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfigaro_cuda.so")
+LIB_PATH = os.environ.get("FG_LIB") or os.path.join(_HERE, "lib", "libfigaro_cuda.so")
 
 FG_OK = 0
 FG_E_ARG, FG_E_SCHEMA, FG_E_TREE, FG_E_INTEGRITY, FG_E_SIZE = 1, 2, 3, 4, 5

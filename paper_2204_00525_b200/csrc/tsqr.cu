@@ -318,6 +318,9 @@ using W16g = WCfg<16, 4, 8, 2, 1>;
 using W32 = WCfg<32, 2, 8, 2>;
 using W12 = WCfg<12, 3, 8, 2>;
 using W20 = WCfg<20, 5, 8, 1>;
+using W20a = WCfg<20, 5, 4, 2>;
+using W20b = WCfg<20, 5, 16, 1>;
+using W20c = WCfg<20, 5, 8, 1, 1>;
 using W24 = WCfg<24, 3, 8, 2>;
 using W32c = WCfg<32, 4, 8, 2>;
 using C16 = Cfg<16, 8, 16, 16>;
@@ -331,7 +334,8 @@ using C32 = Cfg<32, 16, 16, 8>;
 // warpc | cta) -- a tuning knob; the default is the measured best.
 int variant(int W) {
   const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32"
-                         : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128" : "FG_TSQR_X");
+                         : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128"
+                         : W == 20 ? "FG_TSQR_W20" : "FG_TSQR_X");
   if (!e) return W == 16 ? 2 : W == 32 ? 3 : 0;  // measured best (tsqr_sweep.py)
   const std::string v = e;
   if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : v == "blk" ? 3 : v == "blk64" ? 4 : 0;
@@ -394,7 +398,11 @@ Plan plan_for(Context& ctx, int W) {
                     : plan_warp<W32>(ctx);
     }
     case 12: return plan_warp<W12>(ctx);
-    case 20: return plan_warp<W20>(ctx);
+    case 20: {
+      const int v = variant(20);
+      return v == 1 ? plan_warp<W20a>(ctx) : v == 2 ? plan_warp<W20b>(ctx)
+             : v == 3 ? plan_warp<W20c>(ctx) : plan_warp<W20>(ctx);
+    }
     case 24: return plan_warp<W24>(ctx);
     case 64: {
       const int v = variant(64);
@@ -437,7 +445,14 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       break;
     }
     case 12: k_tsqr_warp<W12><<<grid, W12::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 20: k_tsqr_warp<W20><<<grid, W20::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 20: {
+      const int v = variant(20);
+      if (v == 1) k_tsqr_warp<W20a><<<grid, W20a::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 2) k_tsqr_warp<W20b><<<grid, W20b::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 3) k_tsqr_warp<W20c><<<grid, W20c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      else k_tsqr_warp<W20><<<grid, W20::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      break;
+    }
     case 24: k_tsqr_warp<W24><<<grid, W24::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
     case 64: {
       const int v = variant(64);

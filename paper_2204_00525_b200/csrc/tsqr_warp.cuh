@@ -59,6 +59,34 @@ __device__ __forceinline__ Reflector make_reflector(double alpha, double sig) {
   return h;
 }
 
+// The same for callers whose whole warp holds identical (alpha, sig) -- the
+// register kernels broadcast both -- so the range test is a warp vote and
+// the branch is uniform.
+__device__ __forceinline__ Reflector make_reflector_warp(double alpha, double sig) {
+  Reflector h;
+  const double q = fma(alpha, alpha, sig);
+  const bool live = sig > 0.0;
+  const double aa = fabs(alpha);
+  double nrm, t1, t2;
+  if (__all_sync(0xffffffffu, q > 1e-250 && q < 1e250)) {
+    t1 = fast_rsqrt(q);
+    nrm = q * t1;
+    t2 = fast_rcp(nrm + aa);
+  } else {
+    nrm = sqrt(q);
+    t1 = 1.0 / nrm;
+    t2 = 1.0 / (nrm + aa);
+  }
+  h.beta = live ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
+  h.u0 = alpha - h.beta;
+  h.t1 = live ? t1 : 0.0;
+  h.t2 = live ? t2 : 0.0;
+  return h;
+}
+
+#ifndef FG_NCH
+#define FG_NCH 4
+#endif
 // ROLL_ = 1 keeps only the column-block loop unrolled in absorb_tile (the
 // TC steps inside a block run as a loop): ~1/TC of the code, for kernels
 // whose straight-line body overflows the instruction cache.
@@ -102,17 +130,20 @@ __device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
   const int ck = (QB & 1) ? C::TC - 1 - within : within;
   const int rk = k % C::TR;   // lane row holding accumulator row k
   const int mk = k / C::TR;
+  constexpr int NCH = FG_NCH < C::RPT ? FG_NCH : C::RPT;
   double v[C::RPT];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  double sa[NCH];
 #pragma unroll
   for (int i = 0; i < C::RPT; ++i) {
     v[i] = __shfl_sync(0xffffffffu, X[i][QB], r + ck * C::TR);
-    if ((i & 3) == 0) s0 = fma(v[i], v[i], s0);
-    else if ((i & 3) == 1) s1 = fma(v[i], v[i], s1);
-    else if ((i & 3) == 2) s2 = fma(v[i], v[i], s2);
-    else s3 = fma(v[i], v[i], s3);
+    if (i < NCH) sa[i] = v[i] * v[i];
+    else sa[i % NCH] = fma(v[i], v[i], sa[i % NCH]);
   }
-  const double sig = wgroup_sum<C>((s0 + s1) + (s2 + s3));
+#pragma unroll
+  for (int w = NCH / 2; w; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) sa[i] += sa[i + w];
+  const double sig = wgroup_sum<C>(sa[0]);
   // Racc[mk][q] for a possibly run-time mk: a select chain over RR rows.
   auto racc = [&](int q) {
     double x = Racc[0][q];
@@ -122,7 +153,7 @@ __device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
     return x;
   };
   const double alpha = __shfl_sync(0xffffffffu, racc(QB), rk + ck * C::TR);
-  const Reflector h = make_reflector(alpha, sig);
+  const Reflector h = make_reflector_warp(alpha, sig);
   if constexpr (REC) {
     // Reflector k for the caller's block update: {u0, t1, t2}.
     if ((threadIdx.x & 31) == 0) {
@@ -133,16 +164,19 @@ __device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
   }
 #pragma unroll
   for (int q = QB; q < C::CPT; ++q) {
-    const bool act = cols[q] > k;
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    // Slots past the pivot block hold only columns > k.
+    const bool act = q > QB || cols[q] > k;
+    double da[NCH];
 #pragma unroll
     for (int i = 0; i < C::RPT; ++i) {
-      if ((i & 3) == 0) d0 = fma(v[i], X[i][q], d0);
-      else if ((i & 3) == 1) d1 = fma(v[i], X[i][q], d1);
-      else if ((i & 3) == 2) d2 = fma(v[i], X[i][q], d2);
-      else d3 = fma(v[i], X[i][q], d3);
+      if (i < NCH) da[i] = v[i] * X[i][q];
+      else da[i % NCH] = fma(v[i], X[i][q], da[i % NCH]);
     }
-    double d = (d0 + d1) + (d2 + d3);
+#pragma unroll
+    for (int w = NCH / 2; w; w >>= 1)
+#pragma unroll
+      for (int i = 0; i < w; ++i) da[i] += da[i + w];
+    double d = da[0];
     const double rq = racc(q);
     if (r == rk) d = fma(h.u0, rq, d);
     const double dsum = wgroup_sum<C>(d);  // all lanes shuffle
