@@ -21,6 +21,11 @@
 //        random_acyclic_database (testbench.hpp:164), already reduced.
 //   ground_truth P Q N1 N2 SEED OUT.fgdb OUT_RFIXED.bin
 //        generate_ground_truth (testbench.hpp:51).
+//   csv CONFIG OUT.fgrm OUT.txt
+//        load_database (join_tree.hpp:432) of a config + CSV files, then
+//        run_pipeline with semi-join reduction: R (FGRM) and a text dump of
+//        the loaded, canonicalised relations ("name|keys|data" per row, keys
+//        as written in the CSV, data as %.17g).
 //   q IN.fgdb IN.fgrs OUT.fgrq [--cap N]
 //        recover_q (postprocess.hpp:293) with the R stored in IN.fgrs, on the
 //        relations as read (not canonicalised): every streamed (a_row, q_row)
@@ -304,6 +309,47 @@ int cmd_ground_truth(int argc, char** argv) {
   return 0;
 }
 
+int cmd_csv(int argc, char** argv) {
+  if (argc < 5) throw std::runtime_error("csv CONFIG OUT.fgrm OUT.txt");
+  std::ifstream cfg_in(argv[2]);
+  if (!cfg_in) throw std::runtime_error("cannot open config");
+  const std::string cfg_path = argv[2];
+  const auto slash = cfg_path.find_last_of('/');
+  const std::string base = slash == std::string::npos ? "" : cfg_path.substr(0, slash);
+  DatabaseConfig cfg = parse_config(cfg_in);
+  Database db = load_database(cfg, base);
+  {
+    std::ofstream txt(argv[4]);
+    for (const auto& rel : db.relations)
+      for (std::size_t i = 0; i < rel.row_count(); ++i) {
+        txt << rel.name << '|';
+        for (std::size_t c = 0; c < rel.keys[i].size(); ++c) {
+          if (c) txt << ';';
+          const auto& v = rel.keys[i][c];
+          if (std::holds_alternative<std::int64_t>(v)) txt << std::get<std::int64_t>(v);
+          else txt << std::get<std::string>(v);
+        }
+        txt << '|';
+        for (std::size_t c = 0; c < rel.data.cols(); ++c) {
+          if (c) txt << ';';
+          char buf[40];
+          std::snprintf(buf, sizeof buf, "%.17g", rel.data(i, c));
+          txt << buf;
+        }
+        txt << '\n';
+      }
+  }
+  PipelineOptions opts;
+  opts.threads = 1;
+  PipelineResult res = run_pipeline(db.relations, db.tree, opts);
+  Writer w(argv[3]);
+  w.arr("FGRM0001", 8);
+  w.put<std::uint64_t>(res.factor.r.rows());
+  w.arr(res.factor.r.data(), res.factor.r.rows() * res.factor.r.cols());
+  std::printf("ok N=%zu\n", res.factor.r.rows());
+  return 0;
+}
+
 int cmd_q(int argc, char** argv) {
   if (argc < 5) throw std::runtime_error("q IN.fgdb IN.fgrs OUT.fgrq [--cap N]");
   Db db = read_db(argv[2]);
@@ -351,6 +397,7 @@ int main(int argc, char** argv) {
     if (mode == "random") return cmd_random(argc, argv);
     if (mode == "ground_truth") return cmd_ground_truth(argc, argv);
     if (mode == "q") return cmd_q(argc, argv);
+    if (mode == "csv") return cmd_csv(argc, argv);
     throw std::runtime_error("unknown mode " + mode);
   } catch (const integrity_error& e) {
     std::fprintf(stderr, "figaro_ref: integrity_error: %s\n", e.what());
@@ -358,6 +405,12 @@ int main(int argc, char** argv) {
   } catch (const size_error& e) {
     std::fprintf(stderr, "figaro_ref: size_error: %s\n", e.what());
     return 4;
+  } catch (const parse_error& e) {
+    std::fprintf(stderr, "figaro_ref: parse_error: %s\n", e.what());
+    return 6;
+  } catch (const schema_error& e) {
+    std::fprintf(stderr, "figaro_ref: schema_error: %s\n", e.what());
+    return 7;
   } catch (const rank_error& e) {
     std::fprintf(stderr, "figaro_ref: rank_error: %s\n", e.what());
     return 5;
