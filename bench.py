@@ -297,6 +297,8 @@ def main():
             kern["headtail_launches"] += res.headtail_launches
         e1.record(stream)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     launches = ctx.kernel_launches() - k0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
