@@ -157,13 +157,6 @@ __global__ void k_seg_sizes(const int* __restrict__ begins, int64_t G,
 
 __global__ void k_set_last(int* begins, int64_t G, int n) { begins[G] = n; }
 
-__global__ void k_narrow(const uint64_t* __restrict__ in, int64_t n,
-                         uint32_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = static_cast<uint32_t>(in[i]);
-}
-
 __global__ void k_widen(const uint32_t* __restrict__ in, int64_t n,
                         uint64_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -365,6 +358,26 @@ void group_begin(Context& ctx, const uint64_t* keys, int64_t n, int bits,
 void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
                    const int* perm_in, GroupOut& out, GroupPending& pend) {
   group_begin_t<uint32_t>(ctx, keys, n, bits, perm_in, out, pend);
+}
+
+void group_begin_presorted(Context& ctx, const uint64_t* keys, int64_t n,
+                           const int* perm_in, GroupOut& out, GroupPending& pend) {
+  out.perm.alloc(n, ctx.stream);
+  pend.n = n;
+  pend.wide = true;
+  pend.sorted64.alloc(n, ctx.stream);
+  if (n) {
+    FG_CUDA(cudaMemcpyAsync(out.perm.get(), perm_in, n * sizeof(int),
+                            cudaMemcpyDeviceToDevice, ctx.stream));
+    FG_CUDA(cudaMemcpyAsync(pend.sorted64.get(), keys, n * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, ctx.stream));
+  }
+  pend.uniq64.alloc(n, ctx.stream);
+  pend.counts.alloc(n + 1, ctx.stream);
+  pend.nr.alloc(1, ctx.stream);
+  if (n) run_length<uint64_t>(ctx, pend.sorted64.get(), n, pend.uniq64.get(),
+                              pend.counts.get(), pend.nr.get());
+  else pend.nr.zero();
 }
 
 template <class KeyT>

@@ -58,6 +58,9 @@ void group_begin(Context& ctx, const uint64_t* keys, int64_t n, int bits,
 void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
                    const int* perm_in, GroupOut& out, GroupPending& pend);
 void group_finish(Context& ctx, int64_t G, GroupOut& out, GroupPending& pend);
+// Same for keys already in ascending order (no sort; perm_in is kept).
+void group_begin_presorted(Context& ctx, const uint64_t* keys, int64_t n,
+                           const int* perm_in, GroupOut& out, GroupPending& pend);
 // Same with 32-bit packed keys (own keys of <= 32 significant bits).
 void group_sorted32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
                     const int* perm_in, GroupOut& out, bool keep_sorted = false);

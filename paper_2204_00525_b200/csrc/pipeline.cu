@@ -453,7 +453,15 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       piotas[ni].alloc(G, st);
       launch_iota(ctx, piotas[ni].get(), G);
       ppend[ni].keep_sorted = true;
-      group_begin(ctx, ppks[ni].get(), G, pbits, piotas[ni].get(), pgs[ni], ppend[ni]);
+      // Parent attributes that are the leading own-key attributes (in the
+      // same order) project the ascending own keys to ascending parent
+      // keys: no sort needed (C3's F under D1, C4's R2 under R1, 2-way joins).
+      const bool prefix = n.pattr.size() <= n.key_attr.size() &&
+                          std::equal(n.pattr.begin(), n.pattr.end(), n.key_attr.begin());
+      if (prefix)
+        group_begin_presorted(ctx, ppks[ni].get(), G, piotas[ni].get(), pgs[ni], ppend[ni]);
+      else
+        group_begin(ctx, ppks[ni].get(), G, pbits, piotas[ni].get(), pgs[ni], ppend[ni]);
     }
     std::vector<int64_t> Ps(nodes.size(), 0);
     bool any = false;
