@@ -171,6 +171,7 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
+  cudaStream_t copy_stream = nullptr;  // host -> device uploads (run_pipeline)
   int sm_count = 148;
   size_t smem_optin = 0;
   std::string last_error = "ok";

@@ -274,6 +274,26 @@ struct KernelTimer {
   }
 };
 
+// Events of the overlapped host upload (copy stream -> compute stream).
+struct UploadEvents {
+  cudaEvent_t ready = nullptr, keys = nullptr;
+  std::vector<cudaEvent_t> data;
+  cudaStream_t copy = nullptr;  // drained before the buffers are released
+  void init(int n, cudaStream_t s) {
+    copy = s;
+    FG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    FG_CUDA(cudaEventCreateWithFlags(&keys, cudaEventDisableTiming));
+    data.assign(n, nullptr);
+    for (auto& e : data) FG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~UploadEvents() {
+    if (copy) cudaStreamSynchronize(copy);
+    if (ready) cudaEventDestroy(ready);
+    if (keys) cudaEventDestroy(keys);
+    for (auto e : data) if (e) cudaEventDestroy(e);
+  }
+};
+
 struct Events {
   cudaEvent_t e[6];
   Events() { for (auto& x : e) cudaEventCreate(&x); }
@@ -327,25 +347,45 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   KernelTimer kt_ht(st), kt_tsqr(st);
   FG_CUDA(cudaEventRecord(ev.e[0], st));
 
-  // Inputs on the device.
+  // Inputs on the device.  Host inputs are uploaded on the context's copy
+  // stream -- all keys first, then the data in the order the transform reads
+  // it (reverse pre-order) -- so grouping and counts run while the data is
+  // still crossing PCIe; the compute stream waits per relation.
+  UploadEvents up;
+  const bool host_in = opt.memory == FG_MEM_HOST;
+  if (host_in) {
+    for (int i = 0; i < n_rel; ++i) {
+      nodes[i]->keys_own.alloc(rels[i].rows * rels[i].n_key, st);
+      nodes[i]->data_own.alloc(rels[i].rows * rels[i].n_data, st);
+    }
+    up.init(n_rel, ctx.copy_stream);
+    FG_CUDA(cudaEventRecord(up.ready, st));  // buffers free on the compute stream
+    FG_CUDA(cudaStreamWaitEvent(ctx.copy_stream, up.ready, 0));
+  }
   for (int i = 0; i < n_rel; ++i) {
     NodeState& n = *nodes[i];
     const fg_relation& r = rels[i];
-    if (opt.memory == FG_MEM_HOST) {
-      n.keys_own.alloc(r.rows * r.n_key, st);
-      n.data_own.alloc(r.rows * r.n_data, st);
+    if (host_in) {
       if (n.keys_own.size())
         FG_CUDA(cudaMemcpyAsync(n.keys_own.get(), r.keys, n.keys_own.bytes(),
-                                cudaMemcpyHostToDevice, st));
-      if (n.data_own.size())
-        FG_CUDA(cudaMemcpyAsync(n.data_own.get(), r.data, n.data_own.bytes(),
-                                cudaMemcpyHostToDevice, st));
+                                cudaMemcpyHostToDevice, ctx.copy_stream));
       n.keys = n.keys_own.get();
       n.data = n.data_own.get();
     } else {
       n.keys = r.keys;
       n.data = r.data;
     }
+  }
+  if (host_in) {
+    FG_CUDA(cudaEventRecord(up.keys, ctx.copy_stream));
+    for (auto it = preorder.rbegin(); it != preorder.rend(); ++it) {
+      NodeState& n = *nodes[*it];
+      if (n.data_own.size())
+        FG_CUDA(cudaMemcpyAsync(n.data_own.get(), rels[*it].data, n.data_own.bytes(),
+                                cudaMemcpyHostToDevice, ctx.copy_stream));
+      FG_CUDA(cudaEventRecord(up.data[*it], ctx.copy_stream));
+    }
+    FG_CUDA(cudaStreamWaitEvent(st, up.keys, 0));
   }
   FG_CUDA(cudaEventRecord(ev.e[1], st));
   ctx.status.zero();
@@ -576,6 +616,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     const bool fuse = opt.fuse && !opt.keep_r0 && fused_width(n.w) > 0 && n_tails > 0 &&
                       n_tails * 10 >= n.rows * 7;
     if (n.w > 0 && n_tails > 0 && !fuse) n.tails.alloc(n_tails * n.w, st);
+    if (host_in) FG_CUDA(cudaStreamWaitEvent(st, up.data[i], 0));
     HeadTailArgs a;
     a.data = n.data;
     a.ld = n.w;
@@ -841,6 +882,7 @@ fg_status fg_ctx_create(int32_t device, fg_ctx** out) {
     ctx->sm_count = prop.multiProcessorCount;
     ctx->smem_optin = prop.sharedMemPerBlockOptin;
     FG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    FG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     // Keep freed pool memory: no OS round trips in steady state.
     cudaMemPool_t pool;
     FG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -871,6 +913,10 @@ fg_status fg_ctx_destroy(fg_ctx* c) {
   ctx->cache.trim();
   fg::current_cache() = nullptr;
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   delete ctx;
   return FG_OK;
 }
