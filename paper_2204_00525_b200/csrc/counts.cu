@@ -74,6 +74,46 @@ __device__ __forceinline__ void add_runs(uint64_t* table, int64_t slot, uint64_t
   }
 }
 
+// Warp-aggregated checked add for unsorted targets: lanes with equal `slot`
+// (__match_any_sync) are summed by a log-depth peer reduction and the lowest
+// lane of each peer set issues one atomic.  Zipf-distributed child keys make
+// many lanes of a warp hit the same hot entry.
+__device__ __forceinline__ void add_peers(uint64_t* table, int slot, uint64_t v, bool live,
+                                          unsigned* status, bool shared_table = false) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned peers0 = __match_any_sync(full, live ? slot : -1);
+  unsigned long long x = live ? v : 0ull;
+  int ovf = 0;
+  int rel = __popc(peers0 & ((1u << lane) - 1u));  // peers below this lane
+  unsigned peers = peers0 & ~((2u << lane) - 1u);  // peers above this lane
+  if (lane == 31) peers = 0;
+  while (__any_sync(full, peers != 0)) {
+    const int next = __ffs(peers);
+    const unsigned long long t = __shfl_sync(full, x, next ? next - 1 : lane);
+    const int to = __shfl_sync(full, ovf, next ? next - 1 : lane);
+    if ((rel & 1) == 0 && next) {
+      const unsigned long long s2 = x + t;
+      if (s2 < x) ovf = 1;
+      x = s2;
+      ovf |= to;
+    }
+    const unsigned done = __ballot_sync(full, rel & 1);
+    peers &= ~done;
+    rel >>= 1;
+  }
+  if (live && lane == __ffs(peers0) - 1) {
+    if (ovf) atomicOr(status, ST_OVERFLOW);
+    if (shared_table) {
+      const unsigned long long old =
+          atomicAdd(reinterpret_cast<unsigned long long*>(table + slot), x);
+      if (old + x < old) atomicOr(status, ST_OVERFLOW);
+    } else {
+      add_chk(&table[slot], x, status);
+    }
+  }
+}
+
 __global__ void k_theta(const uint64_t* __restrict__ sizes, int64_t G,
                         ChildLinks ch, const int* __restrict__ pidx,
                         uint64_t* phi_down, uint64_t* __restrict__ theta,
@@ -125,7 +165,7 @@ __global__ void k_fjs(const uint64_t* __restrict__ sizes,
     }
     for (int c = 0; c < ch.n; ++c) {
       const int q = live ? ch.lidx[c][k] : -1;
-      add_runs(ch.phi_up[c], q, f, live && q >= 0, status);
+      add_peers(ch.phi_up[c], q, f, live && q >= 0, status);
     }
   }
 }
@@ -138,20 +178,19 @@ __global__ void k_scatter_priv(const uint64_t* __restrict__ fjs, int64_t G,
                                const int* __restrict__ lidx, uint64_t* table,
                                int P, unsigned* status) {
   __shared__ unsigned long long loc[kPrivMax];
-  __shared__ int ovf;
+  __shared__ unsigned sst;
   for (int i = threadIdx.x; i < P; i += blockDim.x) loc[i] = 0ull;
-  if (threadIdx.x == 0) ovf = 0;
+  if (threadIdx.x == 0) sst = 0;
   __syncthreads();
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < G;
+  const int64_t Gw = (G + 31) & ~int64_t(31);  // warp-uniform trip count
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < Gw;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int q = lidx[k];
-    if (q < 0) continue;
-    const unsigned long long v = fjs[k];
-    const unsigned long long old = atomicAdd(&loc[q], v);
-    if (old + v < old) ovf = 1;
+    const int q = k < G ? lidx[k] : -1;
+    const uint64_t v = q >= 0 ? fjs[k] : 0ull;
+    add_peers(reinterpret_cast<uint64_t*>(loc), q, v, q >= 0, &sst, true);
   }
   __syncthreads();
-  if (threadIdx.x == 0 && ovf) atomicOr(status, ST_OVERFLOW);
+  if (threadIdx.x == 0 && sst) atomicOr(status, sst);
   for (int i = threadIdx.x; i < P; i += blockDim.x)
     if (loc[i]) add_chk(&table[i], loc[i], status);
 }

@@ -113,6 +113,25 @@ __global__ void k_lookup(const uint64_t* __restrict__ own, int64_t n,
   }
 }
 
+// Dense variant for narrow keys: table index by direct addressing.
+__global__ void k_dense_fill(const uint64_t* __restrict__ table, int64_t m,
+                             int* __restrict__ dense) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x)
+    dense[table[j]] = static_cast<int>(j);
+}
+
+__global__ void k_lookup_dense(const uint64_t* __restrict__ own, int64_t n, PackSpec s,
+                               const int* __restrict__ dense, int* __restrict__ out,
+                               unsigned* status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = dense[project_one(own[i], s)];
+    out[i] = j;
+    if (j < 0) atomicOr(status, ST_MISSING_CHILD);
+  }
+}
+
 __global__ void k_unpack(const uint64_t* __restrict__ in, int64_t n,
                          PackSpec s, int64_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -201,6 +220,25 @@ void launch_lookup(Context& ctx, const uint64_t* own_keys, int64_t n,
   if (n == 0) return;
   k_lookup<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(own_keys, n, proj,
                                                           table, m, out, status);
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
+}
+
+void launch_lookup_bits(Context& ctx, const uint64_t* own_keys, int64_t n,
+                        const PackSpec& proj, const uint64_t* table, int64_t m,
+                        int bits, int* out, unsigned* status) {
+  if (n == 0) return;
+  if (bits > 24 || m == 0) {
+    launch_lookup(ctx, own_keys, n, proj, table, m, out, status);
+    return;
+  }
+  DevArray<int> dense(size_t(1) << bits, ctx.stream);
+  FG_CUDA(cudaMemsetAsync(dense.get(), 0xff, dense.bytes(), ctx.stream));  // -1
+  k_dense_fill<<<grid_for(ctx, m), kThreads, 0, ctx.stream>>>(table, m, dense.get());
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
+  k_lookup_dense<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(own_keys, n, proj,
+                                                                dense.get(), out, status);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
 }

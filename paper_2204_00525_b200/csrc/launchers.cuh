@@ -86,6 +86,11 @@ void launch_run_ids(Context& ctx, const uint64_t* sorted, const int* perm,
 void launch_lookup(Context& ctx, const uint64_t* own_keys, int64_t n,
                    const PackSpec& proj, const uint64_t* table, int64_t m,
                    int* out, unsigned* status);
+// Same with the table's key width: keys of <= 24 bits use a direct-address
+// table (one gather instead of a binary search).
+void launch_lookup_bits(Context& ctx, const uint64_t* own_keys, int64_t n,
+                        const PackSpec& proj, const uint64_t* table, int64_t m,
+                        int bits, int* out, unsigned* status);
 // Decodes packed keys back to int64 tuples (n x spec.n).
 void launch_unpack(Context& ctx, const uint64_t* in, int64_t n,
                    const PackSpec& spec, int64_t* out);

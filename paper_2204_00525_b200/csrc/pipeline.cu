@@ -537,6 +537,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     NodeState& n = *np;
     for (int c : n.children) {
       NodeState& ch = *nodes[c];
+      int pbits = 0;
       PackSpec proj = make_spec(ch.pattr, code,
                                 [&](int a) {
                                   const int f = (int)(std::find(n.key_attr.begin(),
@@ -544,10 +545,10 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
                                                       n.key_attr.begin());
                                   return n.own.shift[f];
                                 },
-                                nullptr, "edge " + n.name + "-" + ch.name);
+                                &pbits, "edge " + n.name + "-" + ch.name);
       DevArray<int> l(n.grp.G, st);
-      launch_lookup(ctx, n.grp.uniq.get(), n.grp.G, proj, ch.upk.get(), ch.P,
-                    l.get(), ctx.status.get());
+      launch_lookup_bits(ctx, n.grp.uniq.get(), n.grp.G, proj, ch.upk.get(), ch.P,
+                         pbits, l.get(), ctx.status.get());
       n.lidx.push_back(std::move(l));
     }
   }
