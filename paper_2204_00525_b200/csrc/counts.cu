@@ -156,11 +156,21 @@ __global__ void k_fjs(const uint64_t* __restrict__ sizes,
       f = mul_chk(theta[k], up, status);
       fjs[k] = f;
       const uint64_t m = sizes[k];
-      if (m == 0 || f % m != 0) {
+      // exact_div (counts.hpp:64-71): 32-bit hardware path when both fit.
+      uint64_t q, r;
+      if (((f | m) >> 32) == 0) {
+        const unsigned q32 = (unsigned)f / (unsigned)m;
+        q = q32;
+        r = (unsigned)f - q32 * (unsigned)m;
+      } else {
+        q = m ? f / m : 0;
+        r = m ? f - q * m : 1;
+      }
+      if (m == 0 || r != 0) {
         atomicOr(status, ST_CIRC_INEXACT);
         circ[k] = 0;
       } else {
-        circ[k] = f / m;
+        circ[k] = q;
       }
     }
     for (int c = 0; c < ch.n; ++c) {

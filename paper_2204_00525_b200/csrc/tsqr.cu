@@ -329,6 +329,8 @@ using B32s = BCfg<32, 64>;
 using B64 = BCfg<64, 128>;
 using B64s = BCfg<64, 64>;
 using C32 = Cfg<32, 16, 16, 8>;
+using C40 = Cfg<40, 20, 8, 16>;
+using C48 = Cfg<48, 24, 8, 16>;
 
 // Kernel variant per width (FG_TSQR_W16 / FG_TSQR_W32 = warp | warpb |
 // warpc | cta) -- a tuning knob; the default is the measured best.
@@ -344,7 +346,7 @@ int variant(int W) {
 }
 
 int bucket(int w) {
-  for (int b : {4, 8, 12, 16, 20, 24, 32, 64, 128})
+  for (int b : {4, 8, 12, 16, 20, 24, 32, 40, 48, 64, 128})
     if (w <= b) return b;
   return 0;
 }
@@ -404,6 +406,8 @@ Plan plan_for(Context& ctx, int W) {
              : v == 3 ? plan_warp<W20c>(ctx) : plan_warp<W20>(ctx);
     }
     case 24: return plan_warp<W24>(ctx);
+    case 40: return plan_cta<C40>(ctx);
+    case 48: return plan_cta<C48>(ctx);
     case 64: {
       const int v = variant(64);
       return v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
@@ -454,6 +458,8 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       break;
     }
     case 24: k_tsqr_warp<W24><<<grid, W24::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 40: k_tsqr<C40><<<grid, C40::NT, C40::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 48: k_tsqr<C48><<<grid, C48::NT, C48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
     case 64: {
       const int v = variant(64);
       if (v == 1) k_tsqr<C64a><<<grid, C64a::NT, C64a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
