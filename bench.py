@@ -310,10 +310,12 @@ def main():
     # e2e: host (pinned) relations through the same public API; H2D of the
     # step's inputs and D2H of R inside the timed region.
     host_rels = []
+    pinned = []
     h2d = 0
     for r in db.relations:
         k = torch.from_numpy(r.keys).pin_memory()
         d = torch.from_numpy(r.data).pin_memory()
+        pinned.append((k, d))
         h2d += k.numel() * 8 + d.numel() * 8
         host_rels.append(F.Relation(r.name, r.key_attrs, r.data_attrs, k.numpy(), d.numpy()))
     F.run_pipeline(host_rels, tree, opts, device=local, fetch_counts=False)
@@ -334,6 +336,24 @@ def main():
         e2e_s = float(t.item())
     e2e = {"value": m_rank * world / e2e_s, "unit": "tuples/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": n * n * 8, "ms_per_step": e2e_s * 1e3}
+    # The e2e roofline: a plain pinned host -> device copy of the same bytes
+    # (best of 3), i.e. the PCIe time no implementation can go below.
+    dev_bufs = [(torch.empty_like(k, device="cuda"), torch.empty_like(d, device="cuda"))
+                for k, d in pinned]
+    best = float("inf")
+    for _ in range(3):
+        torch.cuda.synchronize()
+        c0 = time.perf_counter()
+        for (dk, dd), (k, d) in zip(dev_bufs, pinned):
+            dk.copy_(k, non_blocking=True)
+            dd.copy_(d, non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - c0)
+    del dev_bufs
+    h2d_gbs = h2d / best / 1e9
+    e2e["roofline"] = {"bound": "pcie_h2d", "achieved": h2d / e2e_s / 1e9, "peak": h2d_gbs,
+                       "unit": "GB/s", "frac": (h2d / e2e_s / 1e9) / h2d_gbs,
+                       "peak_source": "measured here: pinned cudaMemcpyAsync of the step's input bytes, best of 3"}
 
     if rank == 0:
         hbm, src = load_peaks()
@@ -357,7 +377,7 @@ def main():
                          "frac": achieved / hbm,
                          "traffic": ncu_traffic("k_heads_tails_tsqr<2, WCfg<16")
                          if args.config == "C2" else None,
-                         "traffic_source": "profiles/ncu_traffic_r1.json (ncu --set full, C2)",
+                         "traffic_source": "profiles/ncu_traffic_r1.json (ncu --set full, C2; summary in profiles/r1s2/ncu_fused_c2.txt)",
                          "algorithmic_bytes_per_launch": ht_bytes / launches_per_step,
                          "launches_per_step": launches_per_step,
                          "ms_per_launch": ht_s / launches_per_step * 1e3,

@@ -243,7 +243,7 @@ def test_cpp_facade_on_reference_types():
     assert "PASS" in out.stdout
 
 
-@pytest.mark.parametrize("w1,w2", [(12, 20), (24, 5), (32, 3), (1, 33), (7, 9), (64, 2)])
+@pytest.mark.parametrize("w1,w2", [(12, 20), (24, 5), (32, 3), (1, 33), (7, 9), (40, 5), (64, 2)])
 @pytest.mark.parametrize("fuse", [True, False])
 def test_widths_cover_every_kernel_shape(w1, w2, fuse, tmp_path, ref_bin):
     """2-relation joins whose widths hit each fused / TSQR bucket (4..128),
