@@ -747,8 +747,8 @@ __global__ void __launch_bounds__(256) k_join_elems(const __grid_constant__ Join
       int c = 0;
       while (c + 1 < nc && j >= a.child_off[c + 1]) ++c;
       const int idx = a.lidx[c][k];
-      if (idx < 0) continue;
-      S[le] = a.child_S[c][(int64_t)idx * a.child_w[c] + (j - a.child_off[c])] * f[c];
+      S[le] = idx < 0 ? 0.0
+                      : a.child_S[c][(int64_t)idx * a.child_w[c] + (j - a.child_off[c])] * f[c];
     }
   }
 }

@@ -607,8 +607,10 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     const bool is_leaf = n.children.empty();
     const int64_t G = n.grp.G;
     n.width = lay.sub_end[i] - lay.sub_begin[i];
+    // Every element of S is written: own columns by the heads (one per
+    // group), child columns by the join (zero for a missing child), so no
+    // memset (8.6 GB on C3's fact node).
     n.S.alloc(G * n.width, st);
-    if (!is_leaf) n.S.zero();
     n.scale.alloc(G, st);
     const int64_t n_tails = n.rows - G;
     // The fused kernel absorbs a zero row per group start; when groups are
