@@ -45,6 +45,7 @@ struct SegDev {
 }  // namespace
 }  // namespace fg
 #include "tsqr_blk.cuh"
+#include "tsqr_la.cuh"
 namespace fg {
 namespace {
 
@@ -329,6 +330,12 @@ using B32s = BCfg<32, 64>;
 using B64 = BCfg<64, 128>;
 using B64s = BCfg<64, 64>;
 using C32 = Cfg<32, 16, 16, 8>;
+using L32 = LCfg<32, 64, 4, 4>;
+using L64 = LCfg<64, 64, 8, 2>;
+using L64b = LCfg<64, 64, 4, 3, 1>;
+using L64c = LCfg<64, 128, 4, 2, 1>;
+using L128 = LCfg<128, 32, 8, 1>;
+using L128b = LCfg<128, 64, 8, 1, 1>;
 using C40 = Cfg<40, 20, 8, 16>;
 using C48 = Cfg<48, 24, 8, 16>;
 
@@ -338,8 +345,13 @@ int variant(int W) {
   const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32"
                          : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128"
                          : W == 20 ? "FG_TSQR_W20" : "FG_TSQR_X");
-  if (!e) return W == 16 ? 2 : W == 32 ? 3 : 0;  // measured best (tsqr_sweep.py)
+  // measured best (scripts/tsqr_sweep.py, scripts/tsqr_variants.py)
+  if (!e) return W == 16 ? 2 : W == 32 ? 3 : (W == 64 || W == 128) ? 11 : 0;
   const std::string v = e;
+  if (v == "la") return 10;
+  if (v == "lab") return 11;
+  if (v == "lac") return 12;
+  if (W >= 64 && v == "cta") return 0;
   if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : v == "blk" ? 3 : v == "blk64" ? 4 : 0;
   return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : v == "warpd" ? 4
          : v == "warpe" ? 5 : v == "warpf" ? 6 : v == "warpg" ? 7 : v == "blk" ? 8 : v == "blk64" ? 9 : 0;
@@ -377,6 +389,10 @@ Plan plan_blk(Context& ctx) {
   return {C::B, 1, resident(ctx, k_tsqr_blk<C, SegDev>, C::NT, C::smem_bytes)};
 }
 template <class C>
+Plan plan_la(Context& ctx) {
+  return {C::B, 1, resident(ctx, k_tsqr_la<C, SegDev>, C::NT, C::smem_bytes)};
+}
+template <class C>
 Plan plan_warp(Context& ctx) {
   return {C::B, C::WARPS, resident(ctx, k_tsqr_warp<C>, C::NT, C::smem_bytes)};
 }
@@ -395,7 +411,7 @@ Plan plan_for(Context& ctx, int W) {
     }
     case 32: {
       const int v = variant(32);
-      return v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
+      return v == 10 ? plan_la<L32>(ctx) : v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
                     : v == 8 ? plan_blk<B32>(ctx) : v == 9 ? plan_blk<B32s>(ctx)
                     : plan_warp<W32>(ctx);
     }
@@ -410,13 +426,13 @@ Plan plan_for(Context& ctx, int W) {
     case 48: return plan_cta<C48>(ctx);
     case 64: {
       const int v = variant(64);
-      return v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
+      return v == 10 ? plan_la<L64>(ctx) : v == 11 ? plan_la<L64b>(ctx) : v == 12 ? plan_la<L64c>(ctx) : v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
              : v == 3 ? plan_blk<B64>(ctx) : v == 4 ? plan_blk<B64s>(ctx)
              : plan_cta<C64>(ctx);
     }
     default: {
       const int v = variant(128);
-      return v == 1 ? plan_cta<C128a>(ctx) : v == 2 ? plan_cta<C128b>(ctx) : plan_cta<C128>(ctx);
+      return v == 10 ? plan_la<L128>(ctx) : v == 11 ? plan_la<L128b>(ctx) : v == 1 ? plan_cta<C128a>(ctx) : v == 2 ? plan_cta<C128b>(ctx) : plan_cta<C128>(ctx);
     }
   }
 }
@@ -441,7 +457,8 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
     }
     case 32: {
       const int v = variant(32);
-      if (v == 2) k_tsqr_warp<W32c><<<grid, W32c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+      if (v == 10) k_tsqr_la<L32, SegDev><<<grid, L32::NT, L32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 2) k_tsqr_warp<W32c><<<grid, W32c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 3) k_tsqr<C32><<<grid, C32::NT, C32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 8) k_tsqr_blk<B32, SegDev><<<grid, B32::NT, B32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 9) k_tsqr_blk<B32s, SegDev><<<grid, B32s::NT, B32s::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
@@ -462,7 +479,10 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
     case 48: k_tsqr<C48><<<grid, C48::NT, C48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
     case 64: {
       const int v = variant(64);
-      if (v == 1) k_tsqr<C64a><<<grid, C64a::NT, C64a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      if (v == 10) k_tsqr_la<L64, SegDev><<<grid, L64::NT, L64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 11) k_tsqr_la<L64b, SegDev><<<grid, L64b::NT, L64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 12) k_tsqr_la<L64c, SegDev><<<grid, L64c::NT, L64c::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 1) k_tsqr<C64a><<<grid, C64a::NT, C64a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 2) k_tsqr<C64b><<<grid, C64b::NT, C64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 3) k_tsqr_blk<B64, SegDev><<<grid, B64::NT, B64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 4) k_tsqr_blk<B64s, SegDev><<<grid, B64s::NT, B64s::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
@@ -471,7 +491,9 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
     }
     default: {
       const int v = variant(128);
-      if (v == 1) k_tsqr<C128a><<<grid, C128a::NT, C128a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      if (v == 10) k_tsqr_la<L128, SegDev><<<grid, L128::NT, L128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 11) k_tsqr_la<L128b, SegDev><<<grid, L128b::NT, L128b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 1) k_tsqr<C128a><<<grid, C128a::NT, C128a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 2) k_tsqr<C128b><<<grid, C128b::NT, C128b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       break;
