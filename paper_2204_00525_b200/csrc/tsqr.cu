@@ -331,6 +331,12 @@ using B64 = BCfg<64, 128>;
 using B64s = BCfg<64, 64>;
 using C32 = Cfg<32, 16, 16, 8>;
 using L32 = LCfg<32, 64, 4, 4>;
+using L32b = LCfg<32, 64, 2, 6, 1>;
+using L32c = LCfg<32, 64, 4, 3, 1>;
+using L40 = LCfg<40, 64, 2, 6, 1>;
+using L48 = LCfg<48, 64, 2, 5, 1>;
+using L40b = LCfg<40, 64, 4, 3, 1>;
+using L48b = LCfg<48, 64, 4, 3, 1>;
 using L64 = LCfg<64, 64, 8, 2>;
 using L64b = LCfg<64, 64, 4, 3, 1>;
 using L64c = LCfg<64, 128, 4, 2, 1>;
@@ -344,12 +350,14 @@ using C48 = Cfg<48, 24, 8, 16>;
 int variant(int W) {
   const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32"
                          : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128"
-                         : W == 20 ? "FG_TSQR_W20" : "FG_TSQR_X");
+                         : W == 20 ? "FG_TSQR_W20" : W == 40 ? "FG_TSQR_W40"
+                         : W == 48 ? "FG_TSQR_W48" : "FG_TSQR_X");
   // measured best (scripts/tsqr_sweep.py, scripts/tsqr_variants.py)
-  if (!e) return W == 16 ? 2 : W == 32 ? 3 : (W == 64 || W == 128) ? 11 : 0;
+  if (!e) return W == 16 ? 2 : (W == 32 || W == 48 || W == 64 || W == 128) ? 11 : 0;
   const std::string v = e;
   if (v == "la") return 10;
   if (v == "lab") return 11;
+  if (W == 40 || W == 48) return v == "lab" ? 11 : v == "lac" ? 12 : 0;
   if (v == "lac") return 12;
   if (W >= 64 && v == "cta") return 0;
   if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : v == "blk" ? 3 : v == "blk64" ? 4 : 0;
@@ -411,7 +419,7 @@ Plan plan_for(Context& ctx, int W) {
     }
     case 32: {
       const int v = variant(32);
-      return v == 10 ? plan_la<L32>(ctx) : v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
+      return v == 10 ? plan_la<L32>(ctx) : v == 11 ? plan_la<L32b>(ctx) : v == 12 ? plan_la<L32c>(ctx) : v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
                     : v == 8 ? plan_blk<B32>(ctx) : v == 9 ? plan_blk<B32s>(ctx)
                     : plan_warp<W32>(ctx);
     }
@@ -422,8 +430,14 @@ Plan plan_for(Context& ctx, int W) {
              : v == 3 ? plan_warp<W20c>(ctx) : plan_warp<W20>(ctx);
     }
     case 24: return plan_warp<W24>(ctx);
-    case 40: return plan_cta<C40>(ctx);
-    case 48: return plan_cta<C48>(ctx);
+    case 40: {
+      const int v = variant(40);
+      return v == 11 ? plan_la<L40>(ctx) : v == 12 ? plan_la<L40b>(ctx) : plan_cta<C40>(ctx);
+    }
+    case 48: {
+      const int v = variant(48);
+      return v == 11 ? plan_la<L48>(ctx) : v == 12 ? plan_la<L48b>(ctx) : plan_cta<C48>(ctx);
+    }
     case 64: {
       const int v = variant(64);
       return v == 10 ? plan_la<L64>(ctx) : v == 11 ? plan_la<L64b>(ctx) : v == 12 ? plan_la<L64c>(ctx) : v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
@@ -458,6 +472,8 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
     case 32: {
       const int v = variant(32);
       if (v == 10) k_tsqr_la<L32, SegDev><<<grid, L32::NT, L32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 11) k_tsqr_la<L32b, SegDev><<<grid, L32b::NT, L32b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 12) k_tsqr_la<L32c, SegDev><<<grid, L32c::NT, L32c::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 2) k_tsqr_warp<W32c><<<grid, W32c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 3) k_tsqr<C32><<<grid, C32::NT, C32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 8) k_tsqr_blk<B32, SegDev><<<grid, B32::NT, B32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
@@ -475,8 +491,20 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       break;
     }
     case 24: k_tsqr_warp<W24><<<grid, W24::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 40: k_tsqr<C40><<<grid, C40::NT, C40::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 48: k_tsqr<C48><<<grid, C48::NT, C48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
+    case 40: {
+      const int v = variant(40);
+      if (v == 11) k_tsqr_la<L40, SegDev><<<grid, L40::NT, L40::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 12) k_tsqr_la<L40b, SegDev><<<grid, L40b::NT, L40b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else k_tsqr<C40><<<grid, C40::NT, C40::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      break;
+    }
+    case 48: {
+      const int v = variant(48);
+      if (v == 11) k_tsqr_la<L48, SegDev><<<grid, L48::NT, L48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 12) k_tsqr_la<L48b, SegDev><<<grid, L48b::NT, L48b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else k_tsqr<C48><<<grid, C48::NT, C48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      break;
+    }
     case 64: {
       const int v = variant(64);
       if (v == 10) k_tsqr_la<L64, SegDev><<<grid, L64::NT, L64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
