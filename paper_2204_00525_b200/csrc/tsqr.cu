@@ -337,28 +337,43 @@ using L40 = LCfg<40, 64, 2, 6, 1>;
 using L48 = LCfg<48, 64, 2, 5, 1>;
 using L40b = LCfg<40, 64, 4, 3, 1>;
 using L48b = LCfg<48, 64, 4, 3, 1>;
+using L48t = LCfg<48, 64, 2, 5, 1, 1>;
 using L64 = LCfg<64, 64, 8, 2>;
 using L64b = LCfg<64, 64, 4, 3, 1>;
 using L64c = LCfg<64, 128, 4, 2, 1>;
+using L64t = LCfg<64, 64, 2, 4, 1, 1>;
+using L64u = LCfg<64, 64, 4, 3, 1, 1>;
 using L128 = LCfg<128, 32, 8, 1>;
 using L128b = LCfg<128, 64, 8, 1, 1>;
+using L128t = LCfg<128, 32, 4, 2, 1, 1>;
+using L128u = LCfg<128, 64, 4, 1, 1, 1>;
 using C40 = Cfg<40, 20, 8, 16>;
 using C48 = Cfg<48, 24, 8, 16>;
 
 // Kernel variant per width (FG_TSQR_W16 / FG_TSQR_W32 = warp | warpb |
 // warpc | cta) -- a tuning knob; the default is the measured best.
-int variant(int W) {
+// Spans of at least this many rows take the 2-warp triangular-R look-ahead
+// kernel at W = 64 / 128 (4 / 2 CTAs per SM); smaller ones (merge levels)
+// the 8-warp one, whose per-tile latency is lower.
+constexpr int64_t kBigSpan = int64_t(1) << 19;
+
+int variant(int W, int64_t rows = 0) {
   const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32"
                          : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128"
                          : W == 20 ? "FG_TSQR_W20" : W == 40 ? "FG_TSQR_W40"
                          : W == 48 ? "FG_TSQR_W48" : "FG_TSQR_X");
   // measured best (scripts/tsqr_sweep.py, scripts/tsqr_variants.py)
-  if (!e) return W == 16 ? 2 : (W == 32 || W == 48 || W == 64 || W == 128) ? 11 : 0;
+  if (!e) {
+    if ((W == 64 || W == 128) && rows >= kBigSpan) return 13;
+    return W == 16 ? 2 : (W == 32 || W == 48 || W == 64 || W == 128) ? 11 : 0;
+  }
   const std::string v = e;
   if (v == "la") return 10;
   if (v == "lab") return 11;
-  if (W == 40 || W == 48) return v == "lab" ? 11 : v == "lac" ? 12 : 0;
+  if (W == 40 || W == 48) return v == "lab" ? 11 : v == "lac" ? 12 : v == "lat" ? 13 : 0;
   if (v == "lac") return 12;
+  if (v == "lat") return 13;
+  if (v == "lau") return 14;
   if (W >= 64 && v == "cta") return 0;
   if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : v == "blk" ? 3 : v == "blk64" ? 4 : 0;
   return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : v == "warpd" ? 4
@@ -405,7 +420,7 @@ Plan plan_warp(Context& ctx) {
   return {C::B, C::WARPS, resident(ctx, k_tsqr_warp<C>, C::NT, C::smem_bytes)};
 }
 
-Plan plan_for(Context& ctx, int W) {
+Plan plan_for(Context& ctx, int W, int64_t rows) {
   switch (W) {
     case 4: return plan_warp<W4>(ctx);
     case 8: return plan_warp<W8>(ctx);
@@ -436,17 +451,19 @@ Plan plan_for(Context& ctx, int W) {
     }
     case 48: {
       const int v = variant(48);
-      return v == 11 ? plan_la<L48>(ctx) : v == 12 ? plan_la<L48b>(ctx) : plan_cta<C48>(ctx);
+      return v == 11 ? plan_la<L48>(ctx) : v == 12 ? plan_la<L48b>(ctx) : v == 13 ? plan_la<L48t>(ctx) : plan_cta<C48>(ctx);
     }
     case 64: {
-      const int v = variant(64);
-      return v == 10 ? plan_la<L64>(ctx) : v == 11 ? plan_la<L64b>(ctx) : v == 12 ? plan_la<L64c>(ctx) : v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
+      const int v = variant(64, rows);
+      return v == 10 ? plan_la<L64>(ctx) : v == 11 ? plan_la<L64b>(ctx) : v == 12 ? plan_la<L64c>(ctx) :
+             v == 13 ? plan_la<L64t>(ctx) : v == 14 ? plan_la<L64u>(ctx) : v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
              : v == 3 ? plan_blk<B64>(ctx) : v == 4 ? plan_blk<B64s>(ctx)
              : plan_cta<C64>(ctx);
     }
     default: {
-      const int v = variant(128);
-      return v == 10 ? plan_la<L128>(ctx) : v == 11 ? plan_la<L128b>(ctx) : v == 1 ? plan_cta<C128a>(ctx) : v == 2 ? plan_cta<C128b>(ctx) : plan_cta<C128>(ctx);
+      const int v = variant(128, rows);
+      return v == 10 ? plan_la<L128>(ctx) : v == 11 ? plan_la<L128b>(ctx) :
+             v == 13 ? plan_la<L128t>(ctx) : v == 14 ? plan_la<L128u>(ctx) : v == 1 ? plan_cta<C128a>(ctx) : v == 2 ? plan_cta<C128b>(ctx) : plan_cta<C128>(ctx);
     }
   }
 }
@@ -502,14 +519,17 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       const int v = variant(48);
       if (v == 11) k_tsqr_la<L48, SegDev><<<grid, L48::NT, L48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 12) k_tsqr_la<L48b, SegDev><<<grid, L48b::NT, L48b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 13) k_tsqr_la<L48t, SegDev><<<grid, L48t::NT, L48t::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else k_tsqr<C48><<<grid, C48::NT, C48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       break;
     }
     case 64: {
-      const int v = variant(64);
+      const int v = variant(64, rows);
       if (v == 10) k_tsqr_la<L64, SegDev><<<grid, L64::NT, L64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 11) k_tsqr_la<L64b, SegDev><<<grid, L64b::NT, L64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 12) k_tsqr_la<L64c, SegDev><<<grid, L64c::NT, L64c::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 13) k_tsqr_la<L64t, SegDev><<<grid, L64t::NT, L64t::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 14) k_tsqr_la<L64u, SegDev><<<grid, L64u::NT, L64u::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 1) k_tsqr<C64a><<<grid, C64a::NT, C64a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 2) k_tsqr<C64b><<<grid, C64b::NT, C64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 3) k_tsqr_blk<B64, SegDev><<<grid, B64::NT, B64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
@@ -518,9 +538,11 @@ void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
       break;
     }
     default: {
-      const int v = variant(128);
+      const int v = variant(128, rows);
       if (v == 10) k_tsqr_la<L128, SegDev><<<grid, L128::NT, L128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 11) k_tsqr_la<L128b, SegDev><<<grid, L128b::NT, L128b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 13) k_tsqr_la<L128t, SegDev><<<grid, L128t::NT, L128t::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+      else if (v == 14) k_tsqr_la<L128u, SegDev><<<grid, L128u::NT, L128u::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 1) k_tsqr<C128a><<<grid, C128a::NT, C128a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else if (v == 2) k_tsqr<C128b><<<grid, C128b::NT, C128b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
       else k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
@@ -545,7 +567,9 @@ struct Partial {
 // factors written to out.
 int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_unit,
            DevArray<double>& out) {
-  const Plan p = plan_for(ctx, W);
+  int64_t all_rows = 0;
+  for (auto& s : segs) all_rows += s.rows;
+  const Plan p = plan_for(ctx, W, all_rows);
   // A unit must absorb more rows than a factor has, or merges cannot shrink.
   tiles_per_unit = std::max<int64_t>(tiles_per_unit, 2 * ceil_div(W, p.B));
   int64_t rows = 0;

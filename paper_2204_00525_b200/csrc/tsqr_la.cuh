@@ -40,7 +40,7 @@
 
 namespace fg {
 
-template <int W_, int B_, int WARPS_, int MINB_, int NBUF_ = 2>
+template <int W_, int B_, int WARPS_, int MINB_, int NBUF_ = 2, int RTRI_ = 0>
 struct LCfg {
   static constexpr int W = W_;
   static constexpr int NP = W / 8;
@@ -50,12 +50,16 @@ struct LCfg {
   static constexpr int NT = 32 * WARPS;
   static constexpr int MINB = MINB_;
   static constexpr int NBUF = NBUF_;  // 2: the next tile is staged during this one
+  // RTRI = 1: R kept as its NP (NP + 1) / 2 upper-triangular 8 x 8 blocks
+  // (half the shared memory of the padded square; more CTAs per SM).
+  static constexpr int RTRI = RTRI_;
   static constexpr int LDX = W + 4;
   static constexpr int LDR = W + 4;
   static_assert(W % 8 == 0 && B % 8 == 0 && WARPS >= 2, "shape");
   static_assert(NBUF == 1 || NBUF == 2, "buffers");
+  static constexpr size_t r_doubles = RTRI ? (size_t)NP * (NP + 1) / 2 * 64 : (size_t)W * LDR;
   static constexpr size_t smem_doubles =
-      (size_t)W * LDR + NBUF * (size_t)B * LDX + 2 * 64 + 2 * 8 + 64 + 64 * WARPS;
+      r_doubles + NBUF * (size_t)B * LDX + 2 * 64 + 2 * 8 + 64 + 64 * WARPS;
   static constexpr size_t smem_bytes = smem_doubles * 8 + B * sizeof(int);
 };
 
@@ -90,6 +94,15 @@ __device__ __noinline__ SRefl srefl_ieee(double alpha, double sig) {
   return h;
 }
 
+// Pointer to R[8p][8j] (j >= p) and the row stride of that block.
+template <class C>
+__device__ __forceinline__ double* rblock(double* R, int p, int j) {
+  if constexpr (C::RTRI) return R + (p * C::NP - p * (p - 1) / 2 + (j - p)) * 64;
+  else return R + 8 * p * C::LDR + 8 * j;
+}
+template <class C>
+constexpr int rld() { return C::RTRI ? 8 : C::LDR; }
+
 __device__ __forceinline__ double qsum_l(double x) {
   x += __shfl_xor_sync(0xffffffffu, x, 1);
   x += __shfl_xor_sync(0xffffffffu, x, 2);
@@ -111,7 +124,7 @@ __device__ __forceinline__ void dm_trailing(double* __restrict__ X, double* __re
     dmma(wa[kk & 3], wb[kk & 3], row[p0 + g], row[J0 + g]);
   }
   const double u = ut[g];
-  double* rp = R + (p0 + g) * C::LDR + J0 + 2 * tg;
+  double* rp = rblock<C>(R, p0 / 8, J0 / 8) + g * rld<C>() + 2 * tg;
   const double r0 = rp[0], r1 = rp[1];
   my[g * 8 + 2 * tg] = fma(u, r0, (wa[0] + wa[1]) + (wa[2] + wa[3]));
   my[g * 8 + 2 * tg + 1] = fma(u, r1, (wb[0] + wb[1]) + (wb[2] + wb[3]));
@@ -151,7 +164,7 @@ __device__ __forceinline__ void la_panel(double* __restrict__ X, double* __restr
   for (int i = 0; i < RPL; ++i) Xp[i] = X[(4 * i + t) * C::LDX + p0 + g];
   double Rd[8];  // R[p0 + i][p0 + g], replicated over the quad
 #pragma unroll
-  for (int i = 0; i < 8; ++i) Rd[i] = R[(p0 + i) * C::LDR + p0 + g];
+  for (int i = 0; i < 8; ++i) Rd[i] = rblock<C>(R, p0 / 8, p0 / 8)[i * rld<C>() + g];
   // exact tail norms of the panel columns
   double sig;
   {
@@ -223,7 +236,7 @@ __device__ __forceinline__ void la_panel(double* __restrict__ X, double* __restr
   for (int i = 0; i < RPL; ++i) X[(4 * i + t) * C::LDX + p0 + g] = Xp[i] * my_s;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
-    if ((i & 3) == t) R[(p0 + i) * C::LDR + p0 + g] = Rd[i];
+    if ((i & 3) == t) rblock<C>(R, p0 / 8, p0 / 8)[i * rld<C>() + g] = Rd[i];
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     if ((k & 3) == t) Gs[g * 8 + k] = k > g ? Gk[k] * my_s : 0.0;
@@ -250,7 +263,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   constexpr int W = C::W, NP = C::NP;
   extern __shared__ __align__(16) double sm[];
   double* R = sm;                                // W x LDR
-  double* Xb0 = R + W * C::LDR;                  // B x LDX (x2)
+  double* Xb0 = R + C::r_doubles;                // B x LDX (x NBUF)
   double* Xb1 = Xb0 + (C::NBUF - 1) * C::B * C::LDX;
   double* Tsb = Xb1 + C::B * C::LDX;             // 2 x (8 x 8), by panel parity
   double* utb = Tsb + 128;                       // 2 x 8
@@ -261,7 +274,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   const int warp = threadIdx.x >> 5;
   double* my = scr + 64 * warp;
 
-  for (int e = threadIdx.x; e < W * C::LDR; e += C::NT) R[e] = 0.0;
+  for (int e = threadIdx.x; e < (int)C::r_doubles; e += C::NT) R[e] = 0.0;
 
   int64_t tt = blockIdx.x;
   if (C::NBUF == 2 && tt < total_tiles) stage_blk<C>(segs, nseg, total_rows, tt, Xb0, rowseg);
@@ -295,7 +308,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   double* o = out + (int64_t)blockIdx.x * W * W;
   for (int e = threadIdx.x; e < W * W; e += C::NT) {
     const int i = e / W, j = e - (e / W) * W;
-    o[e] = R[i * C::LDR + j];
+    o[e] = (j >> 3) < (i >> 3) ? 0.0 : rblock<C>(R, i >> 3, j >> 3)[(i & 7) * rld<C>() + (j & 7)];
   }
 }
 
