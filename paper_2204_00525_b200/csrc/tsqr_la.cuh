@@ -152,8 +152,11 @@ __device__ __forceinline__ void dm_trailing(double* __restrict__ X, double* __re
 
 // Panel p0 of tile X against R (warp 0).  Leaves V~ in X's panel columns,
 // the finished diagonal block in R, u0~ in ut and T in Ts.
+// Returns true (warp-uniform) when the panel's tile columns are all exactly
+// zero: every reflector is the identity, so the panel and every block update
+// it drives are skipped (triangular partial factors stacked in merge levels).
 template <class C>
-__device__ __forceinline__ void la_panel(double* __restrict__ X, double* __restrict__ R,
+__device__ __forceinline__ bool la_panel(double* __restrict__ X, double* __restrict__ R,
                                          int p0, double* __restrict__ Ts,
                                          double* __restrict__ ut, double* __restrict__ Gs,
                                          int lane) {
@@ -176,6 +179,7 @@ __device__ __forceinline__ void la_panel(double* __restrict__ X, double* __restr
     }
     sig = qsum_l(a0 + a1);
   }
+  if (__all_sync(0xffffffffu, sig == 0.0)) return true;
   double smax = sig;
   double sk = __shfl_sync(0xffffffffu, sig, 0);
   double al = __shfl_sync(0xffffffffu, Rd[0], 0);
@@ -254,6 +258,7 @@ __device__ __forceinline__ void la_panel(double* __restrict__ X, double* __restr
   for (int k = 0; k < 8; ++k)
     if ((k & 3) == t) Ts[g * 8 + k] = Tr[k];
   __syncwarp();
+  return false;
 }
 
 template <class C, class Seg>
@@ -268,6 +273,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   double* Tsb = Xb1 + C::B * C::LDX;             // 2 x (8 x 8), by panel parity
   double* utb = Tsb + 128;                       // 2 x 8
   double* Gs = utb + 16;                         // 8 x 8 (warp 0)
+  __shared__ int zpan[2];                        // panel of parity pb is the identity
   double* scr = Gs + 64;                         // 64 per warp
   int* rowseg = reinterpret_cast<int*>(scr + 64 * C::WARPS);
   const int lane = threadIdx.x & 31;
@@ -286,18 +292,24 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     __syncthreads();  // tile tt staged; the other buffer is free
     if (C::NBUF == 2 && tt + nunits < total_tiles)
       stage_blk<C>(segs, nseg, total_rows, tt + nunits, buf ? Xb0 : Xb1, rowseg);
-    if (warp == 0) la_panel<C>(X, R, 0, Tsb, utb, Gs, lane);
+    if (warp == 0) {
+      const bool z = la_panel<C>(X, R, 0, Tsb, utb, Gs, lane);
+      if (lane == 0) zpan[0] = z;
+    }
     __syncthreads();
     for (int p = 0; p < NP; ++p) {
       const int pb = p & 1;
       double* Tp = Tsb + 64 * pb;
       double* up = utb + 8 * pb;
+      const bool zp = zpan[pb];
       if (warp == 0) {
         if (p + 1 < NP) {
-          dm_trailing<C>(X, R, 8 * p, 8 * (p + 1), Tp, up, my, lane);
-          la_panel<C>(X, R, 8 * (p + 1), Tsb + 64 * (pb ^ 1), utb + 8 * (pb ^ 1), Gs, lane);
+          if (!zp) dm_trailing<C>(X, R, 8 * p, 8 * (p + 1), Tp, up, my, lane);
+          const bool z = la_panel<C>(X, R, 8 * (p + 1), Tsb + 64 * (pb ^ 1), utb + 8 * (pb ^ 1),
+                                     Gs, lane);
+          if (lane == 0) zpan[pb ^ 1] = z;
         }
-      } else {
+      } else if (!zp) {
         for (int j = p + 1 + warp; j < NP; j += C::WARPS - 1)
           dm_trailing<C>(X, R, 8 * p, 8 * j, Tp, up, my, lane);
       }
