@@ -365,7 +365,7 @@ int variant(int W, int64_t rows = 0) {
   // measured best (scripts/tsqr_sweep.py, scripts/tsqr_variants.py)
   if (!e) {
     if ((W == 64 || W == 128) && rows >= kBigSpan) return 13;
-    return W == 16 ? 2 : (W == 32 || W == 48 || W == 64 || W == 128) ? 11 : 0;
+    return W == 16 ? 2 : (W == 32 || W == 40 || W == 48 || W == 64 || W == 128) ? 11 : 0;
   }
   const std::string v = e;
   if (v == "la") return 10;

@@ -94,6 +94,36 @@ __device__ __noinline__ SRefl srefl_ieee(double alpha, double sig) {
   return h;
 }
 
+// Stages tile `tile` into X.  Fast path (CTA-uniform): the tile lies inside
+// one dense, 16-byte aligned segment -- 16-byte cp.async with row/column
+// arithmetic only; otherwise the general per-row segment path of stage_blk.
+template <class C, class Seg>
+__device__ __forceinline__ void la_stage(const Seg* __restrict__ segs, int nseg,
+                                         int64_t total_rows, int64_t tile, double* X,
+                                         int* rowseg) {
+  const int64_t r0 = tile * C::B;
+  int lo = 0, hi = nseg;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (segs[mid].row0 <= r0) lo = mid; else hi = mid;
+  }
+  const Seg& sg = segs[lo];
+  const bool fast = r0 + C::B <= sg.row0 + sg.rows && sg.col_begin == 0 && sg.cols == C::W &&
+                    (sg.ld & 1) == 0 && (reinterpret_cast<uintptr_t>(sg.data) & 15) == 0;
+  if (!fast) {
+    stage_blk<C>(segs, nseg, total_rows, tile, X, rowseg);
+    return;
+  }
+  constexpr int HW = C::W / 2;
+  const double* base = sg.data + (r0 - sg.row0) * sg.ld;
+  for (int e = threadIdx.x; e < C::B * HW; e += C::NT) {
+    const int row = e / HW, c2 = e - (e / HW) * HW;
+    __pipeline_memcpy_async(X + row * C::LDX + 2 * c2, base + row * sg.ld + 2 * c2,
+                            2 * sizeof(double));
+  }
+  __pipeline_commit();
+}
+
 // Pointer to R[8p][8j] (j >= p) and the row stride of that block.
 template <class C>
 __device__ __forceinline__ double* rblock(double* R, int p, int j) {
@@ -283,15 +313,15 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   for (int e = threadIdx.x; e < (int)C::r_doubles; e += C::NT) R[e] = 0.0;
 
   int64_t tt = blockIdx.x;
-  if (C::NBUF == 2 && tt < total_tiles) stage_blk<C>(segs, nseg, total_rows, tt, Xb0, rowseg);
+  if (C::NBUF == 2 && tt < total_tiles) la_stage<C>(segs, nseg, total_rows, tt, Xb0, rowseg);
   int buf = 0;
   for (; tt < total_tiles; tt += nunits, buf ^= (C::NBUF - 1)) {
     double* X = buf ? Xb1 : Xb0;
-    if (C::NBUF == 1) stage_blk<C>(segs, nseg, total_rows, tt, X, rowseg);
+    if (C::NBUF == 1) la_stage<C>(segs, nseg, total_rows, tt, X, rowseg);
     __pipeline_wait_prior(0);
     __syncthreads();  // tile tt staged; the other buffer is free
     if (C::NBUF == 2 && tt + nunits < total_tiles)
-      stage_blk<C>(segs, nseg, total_rows, tt + nunits, buf ? Xb0 : Xb1, rowseg);
+      la_stage<C>(segs, nseg, total_rows, tt + nunits, buf ? Xb0 : Xb1, rowseg);
     if (warp == 0) {
       const bool z = la_panel<C>(X, R, 0, Tsb, utb, Gs, lane);
       if (lane == 0) zpan[0] = z;
