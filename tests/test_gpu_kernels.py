@@ -125,3 +125,26 @@ def test_tsqr_rank_deficient_and_empty():
     assert R[1, 1] == 0.0 and R[3, 3] == 0.0
     R = F.tsqr([], 3).cpu().numpy()
     assert np.array_equal(R, np.zeros((3, 3)))
+
+
+@pytest.mark.parametrize("w", [40, 48, 64, 128])
+def test_tsqr_wide_large_spans(w):
+    """The look-ahead blocked TSQR at span sizes that select its large-span
+    configurations (>= 512k rows: triangular-R, 2-warp CTAs at W = 64/128),
+    with exactly zero, duplicated and badly scaled columns (downdate repairs,
+    zero panels).  R is compared through the Gram matrix (rank-deficient)."""
+    rows = 600_000
+    rng = np.random.default_rng(w)
+    x = rng.standard_normal((rows, w)) * np.logspace(-3, 3, w)
+    x[:, 1] = x[:, 0]
+    x[:, w // 2: w // 2 + 8] = 0.0  # one whole zero panel
+    R = F.tsqr([(dev(x), 0)], w).cpu().numpy()
+    assert np.all(np.tril(R, -1) == 0) and np.all(np.diag(R) >= 0)
+    G = x.T @ x
+    assert np.linalg.norm(R.T @ R - G) / np.linalg.norm(G) <= 1e-13
+    # full-rank part: compare with numpy's Householder R on the same columns
+    keep = [j for j in range(w) if j != 1 and not (w // 2 <= j < w // 2 + 8)]
+    xr = np.ascontiguousarray(x[:, keep])
+    Rk = F.tsqr([(dev(xr), 0)], len(keep)).cpu().numpy()
+    ref = fo.normalize_signs(np.linalg.qr(xr, mode="r"))
+    assert r_distance(Rk, ref) <= 1e-12
