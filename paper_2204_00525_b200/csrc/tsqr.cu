@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "launchers.cuh"
 #include "tsqr_warp.cuh"
@@ -301,83 +302,54 @@ __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
   }
 }
 
-using C64 = Cfg<64, 32, 8, 16>;
-using C128 = Cfg<128, 32, 8, 8>;
-using C64a = Cfg<64, 32, 8, 8>;
-using C64b = Cfg<64, 16, 16, 8>;
-using C128a = Cfg<128, 32, 8, 4>;
-using C128b = Cfg<128, 16, 16, 4>;
 using W4 = WCfg<4, 1, 8, 2>;
 using W8 = WCfg<8, 2, 8, 2>;
-using W16 = WCfg<16, 2, 8, 2>;
-using W16b = WCfg<16, 2, 16, 2>;
-using W16c = WCfg<16, 4, 8, 2>;
-using W16d = WCfg<16, 4, 4, 3>;
-using W16e = WCfg<16, 4, 16, 1>;
-using W16f = WCfg<16, 8, 4, 2>;
-using W16g = WCfg<16, 4, 8, 2, 1>;
-using W32 = WCfg<32, 2, 8, 2>;
 using W12 = WCfg<12, 3, 8, 2>;
+using W16 = WCfg<16, 2, 8, 2>;
+using W16c = WCfg<16, 4, 8, 2>;
 using W20 = WCfg<20, 5, 8, 1>;
-using W20a = WCfg<20, 5, 4, 2>;
-using W20b = WCfg<20, 5, 16, 1>;
-using W20c = WCfg<20, 5, 8, 1, 1>;
 using W24 = WCfg<24, 3, 8, 2>;
 using W32c = WCfg<32, 4, 8, 2>;
 using C16 = Cfg<16, 8, 16, 16>;
-using B32 = BCfg<32, 128>;
-using B32s = BCfg<32, 64>;
-using B64 = BCfg<64, 128>;
-using B64s = BCfg<64, 64>;
 using C32 = Cfg<32, 16, 16, 8>;
-using L32 = LCfg<32, 64, 4, 4>;
-using L32b = LCfg<32, 64, 2, 6, 1>;
-using L32c = LCfg<32, 64, 4, 3, 1>;
-using L40 = LCfg<40, 64, 2, 6, 1>;
-using L48 = LCfg<48, 64, 2, 5, 1>;
-using L40b = LCfg<40, 64, 4, 3, 1>;
-using L48b = LCfg<48, 64, 4, 3, 1>;
-using L48t = LCfg<48, 64, 2, 5, 1, 1>;
-using L64 = LCfg<64, 64, 8, 2>;
-using L64b = LCfg<64, 64, 4, 3, 1>;
-using L64c = LCfg<64, 128, 4, 2, 1>;
-using L64t = LCfg<64, 64, 2, 4, 1, 1>;
-using L64u = LCfg<64, 64, 4, 3, 1, 1>;
-using L128 = LCfg<128, 32, 8, 1>;
-using L128b = LCfg<128, 64, 8, 1, 1>;
-using L128t = LCfg<128, 32, 4, 2, 1, 1>;
-using L128u = LCfg<128, 64, 4, 1, 1, 1>;
 using C40 = Cfg<40, 20, 8, 16>;
 using C48 = Cfg<48, 24, 8, 16>;
+using C64 = Cfg<64, 32, 8, 16>;
+using C128 = Cfg<128, 32, 8, 8>;
+// Look-ahead blocked kernels (tsqr_la.cuh): "lab" = single-buffered 64-row
+// tiles, full-square R; "lat" = 2-warp CTAs with triangular-block R (more
+// CTAs per SM, for large spans).
+using L32 = LCfg<32, 64, 2, 6, 1>;
+using L40 = LCfg<40, 64, 2, 6, 1>;
+using L48 = LCfg<48, 64, 2, 5, 1>;
+using L64 = LCfg<64, 64, 4, 3, 1>;
+using L64t = LCfg<64, 64, 2, 4, 1, 1>;
+using L128 = LCfg<128, 64, 8, 1, 1>;
+using L128t = LCfg<128, 32, 4, 2, 1, 1>;
 
-// Kernel variant per width (FG_TSQR_W16 / FG_TSQR_W32 = warp | warpb |
-// warpc | cta) -- a tuning knob; the default is the measured best.
+// Kernel per width.  The default is the measured best
+// (scripts/tsqr_variants.py, profiles/r1s2/tsqr_variants.txt); FG_TSQR_W<W>
+// selects an alternative for experiments: warp | warpc (register warp
+// kernels), cta (column-at-a-time CTA kernel), lab | lat (look-ahead).
+enum class Kern { Warp, WarpC, Cta, La, LaT };
+
 // Spans of at least this many rows take the 2-warp triangular-R look-ahead
 // kernel at W = 64 / 128 (4 / 2 CTAs per SM); smaller ones (merge levels)
-// the 8-warp one, whose per-tile latency is lower.
+// the single-buffered one, whose per-tile latency is lower.
 constexpr int64_t kBigSpan = int64_t(1) << 19;
 
-int variant(int W, int64_t rows = 0) {
-  const char* e = getenv(W == 16 ? "FG_TSQR_W16" : W == 32 ? "FG_TSQR_W32"
-                         : W == 64 ? "FG_TSQR_W64" : W == 128 ? "FG_TSQR_W128"
-                         : W == 20 ? "FG_TSQR_W20" : W == 40 ? "FG_TSQR_W40"
-                         : W == 48 ? "FG_TSQR_W48" : "FG_TSQR_X");
-  // measured best (scripts/tsqr_sweep.py, scripts/tsqr_variants.py)
-  if (!e) {
-    if ((W == 64 || W == 128) && rows >= kBigSpan) return 13;
-    return W == 16 ? 2 : (W == 32 || W == 40 || W == 48 || W == 64 || W == 128) ? 11 : 0;
-  }
-  const std::string v = e;
-  if (v == "la") return 10;
-  if (v == "lab") return 11;
-  if (W == 40 || W == 48) return v == "lab" ? 11 : v == "lac" ? 12 : v == "lat" ? 13 : 0;
-  if (v == "lac") return 12;
-  if (v == "lat") return 13;
-  if (v == "lau") return 14;
-  if (W >= 64 && v == "cta") return 0;
-  if (W >= 64) return v == "a" ? 1 : v == "b" ? 2 : v == "blk" ? 3 : v == "blk64" ? 4 : 0;
-  return v == "warpb" ? 1 : v == "warpc" ? 2 : v == "cta" ? 3 : v == "warpd" ? 4
-         : v == "warpe" ? 5 : v == "warpf" ? 6 : v == "warpg" ? 7 : v == "blk" ? 8 : v == "blk64" ? 9 : 0;
+Kern variant(int W, int64_t rows) {
+  const std::string key = "FG_TSQR_W" + std::to_string(W);
+  const char* e = getenv(key.c_str());
+  const std::string v = e ? e : "";
+  if (v == "warp") return Kern::Warp;
+  if (v == "warpc") return Kern::WarpC;
+  if (v == "cta") return Kern::Cta;
+  if (v == "lab") return Kern::La;
+  if (v == "lat") return Kern::LaT;
+  if (W <= 24) return W == 16 ? Kern::WarpC : Kern::Warp;
+  if ((W == 64 || W == 128) && rows >= kBigSpan) return Kern::LaT;
+  return Kern::La;
 }
 
 int bucket(int w) {
@@ -408,10 +380,6 @@ Plan plan_cta(Context& ctx) {
   return {C::B, 1, resident(ctx, k_tsqr<C>, C::NT, C::smem_bytes)};
 }
 template <class C>
-Plan plan_blk(Context& ctx) {
-  return {C::B, 1, resident(ctx, k_tsqr_blk<C, SegDev>, C::NT, C::smem_bytes)};
-}
-template <class C>
 Plan plan_la(Context& ctx) {
   return {C::B, 1, resident(ctx, k_tsqr_la<C, SegDev>, C::NT, C::smem_bytes)};
 }
@@ -420,135 +388,52 @@ Plan plan_warp(Context& ctx) {
   return {C::B, C::WARPS, resident(ctx, k_tsqr_warp<C>, C::NT, C::smem_bytes)};
 }
 
-Plan plan_for(Context& ctx, int W, int64_t rows) {
+// Runs `f` with the config type of width W / kernel k (unsupported
+// combinations fall back to the width's default kernel family).
+template <class F>
+auto with_kernel(int W, Kern k, F&& f) {
   switch (W) {
-    case 4: return plan_warp<W4>(ctx);
-    case 8: return plan_warp<W8>(ctx);
-    case 16: {
-      const int v = variant(16);
-      return v == 1 ? plan_warp<W16b>(ctx) : v == 2 ? plan_warp<W16c>(ctx)
-             : v == 3 ? plan_cta<C16>(ctx) : v == 4 ? plan_warp<W16d>(ctx)
-             : v == 5 ? plan_warp<W16e>(ctx) : v == 6 ? plan_warp<W16f>(ctx)
-             : v == 7 ? plan_warp<W16g>(ctx)
-             : plan_warp<W16>(ctx);
-    }
-    case 32: {
-      const int v = variant(32);
-      return v == 10 ? plan_la<L32>(ctx) : v == 11 ? plan_la<L32b>(ctx) : v == 12 ? plan_la<L32c>(ctx) : v == 2 ? plan_warp<W32c>(ctx) : v == 3 ? plan_cta<C32>(ctx)
-                    : v == 8 ? plan_blk<B32>(ctx) : v == 9 ? plan_blk<B32s>(ctx)
-                    : plan_warp<W32>(ctx);
-    }
-    case 12: return plan_warp<W12>(ctx);
-    case 20: {
-      const int v = variant(20);
-      return v == 1 ? plan_warp<W20a>(ctx) : v == 2 ? plan_warp<W20b>(ctx)
-             : v == 3 ? plan_warp<W20c>(ctx) : plan_warp<W20>(ctx);
-    }
-    case 24: return plan_warp<W24>(ctx);
-    case 40: {
-      const int v = variant(40);
-      return v == 11 ? plan_la<L40>(ctx) : v == 12 ? plan_la<L40b>(ctx) : plan_cta<C40>(ctx);
-    }
-    case 48: {
-      const int v = variant(48);
-      return v == 11 ? plan_la<L48>(ctx) : v == 12 ? plan_la<L48b>(ctx) : v == 13 ? plan_la<L48t>(ctx) : plan_cta<C48>(ctx);
-    }
-    case 64: {
-      const int v = variant(64, rows);
-      return v == 10 ? plan_la<L64>(ctx) : v == 11 ? plan_la<L64b>(ctx) : v == 12 ? plan_la<L64c>(ctx) :
-             v == 13 ? plan_la<L64t>(ctx) : v == 14 ? plan_la<L64u>(ctx) : v == 1 ? plan_cta<C64a>(ctx) : v == 2 ? plan_cta<C64b>(ctx)
-             : v == 3 ? plan_blk<B64>(ctx) : v == 4 ? plan_blk<B64s>(ctx)
-             : plan_cta<C64>(ctx);
-    }
-    default: {
-      const int v = variant(128, rows);
-      return v == 10 ? plan_la<L128>(ctx) : v == 11 ? plan_la<L128b>(ctx) :
-             v == 13 ? plan_la<L128t>(ctx) : v == 14 ? plan_la<L128u>(ctx) : v == 1 ? plan_cta<C128a>(ctx) : v == 2 ? plan_cta<C128b>(ctx) : plan_cta<C128>(ctx);
-    }
+    case 4: return f(W4{});
+    case 8: return f(W8{});
+    case 12: return f(W12{});
+    case 16: return k == Kern::Cta ? f(C16{}) : k == Kern::Warp ? f(W16{}) : f(W16c{});
+    case 20: return f(W20{});
+    case 24: return f(W24{});
+    case 32: return k == Kern::Cta ? f(C32{}) : (k == Kern::Warp || k == Kern::WarpC) ? f(W32c{}) : f(L32{});
+    case 40: return k == Kern::Cta ? f(C40{}) : f(L40{});
+    case 48: return k == Kern::Cta ? f(C48{}) : f(L48{});
+    case 64: return k == Kern::Cta ? f(C64{}) : k == Kern::LaT ? f(L64t{}) : f(L64{});
+    default: return k == Kern::Cta ? f(C128{}) : k == Kern::LaT ? f(L128t{}) : f(L128{});
   }
+}
+
+template <class C> struct IsWarp : std::false_type {};
+template <int A, int B_, int C_, int D, int E> struct IsWarp<WCfg<A, B_, C_, D, E>> : std::true_type {};
+template <class C> struct IsLa : std::false_type {};
+template <int A, int B_, int C_, int D, int E, int G> struct IsLa<LCfg<A, B_, C_, D, E, G>> : std::true_type {};
+
+Plan plan_for(Context& ctx, int W, int64_t rows) {
+  return with_kernel(W, variant(W, rows), [&](auto cfg) -> Plan {
+    using C = decltype(cfg);
+    if constexpr (IsWarp<C>::value) return plan_warp<C>(ctx);
+    else if constexpr (IsLa<C>::value) return plan_la<C>(ctx);
+    else return plan_cta<C>(ctx);
+  });
 }
 
 void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
                 int64_t rows, int64_t tiles, int64_t units, int grid, double* out) {
   cudaStream_t s = ctx.stream;
-  switch (W) {
-    case 4: k_tsqr_warp<W4><<<grid, W4::NT, W4::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 8: k_tsqr_warp<W8><<<grid, W8::NT, W8::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 16: {
-      const int v = variant(16);
-      if (v == 1) k_tsqr_warp<W16b><<<grid, W16b::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 2) k_tsqr_warp<W16c><<<grid, W16c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 3) k_tsqr<C16><<<grid, C16::NT, C16::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 4) k_tsqr_warp<W16d><<<grid, W16d::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 5) k_tsqr_warp<W16e><<<grid, W16e::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 6) k_tsqr_warp<W16f><<<grid, W16f::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 7) k_tsqr_warp<W16g><<<grid, W16g::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else k_tsqr_warp<W16><<<grid, W16::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      break;
-    }
-    case 32: {
-      const int v = variant(32);
-      if (v == 10) k_tsqr_la<L32, SegDev><<<grid, L32::NT, L32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 11) k_tsqr_la<L32b, SegDev><<<grid, L32b::NT, L32b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 12) k_tsqr_la<L32c, SegDev><<<grid, L32c::NT, L32c::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 2) k_tsqr_warp<W32c><<<grid, W32c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 3) k_tsqr<C32><<<grid, C32::NT, C32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 8) k_tsqr_blk<B32, SegDev><<<grid, B32::NT, B32::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 9) k_tsqr_blk<B32s, SegDev><<<grid, B32s::NT, B32s::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else k_tsqr_warp<W32><<<grid, W32::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      break;
-    }
-    case 12: k_tsqr_warp<W12><<<grid, W12::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 20: {
-      const int v = variant(20);
-      if (v == 1) k_tsqr_warp<W20a><<<grid, W20a::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 2) k_tsqr_warp<W20b><<<grid, W20b::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 3) k_tsqr_warp<W20c><<<grid, W20c::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      else k_tsqr_warp<W20><<<grid, W20::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
-      break;
-    }
-    case 24: k_tsqr_warp<W24><<<grid, W24::NT, 0, s>>>(segs, nseg, rows, tiles, units, out); break;
-    case 40: {
-      const int v = variant(40);
-      if (v == 11) k_tsqr_la<L40, SegDev><<<grid, L40::NT, L40::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 12) k_tsqr_la<L40b, SegDev><<<grid, L40b::NT, L40b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else k_tsqr<C40><<<grid, C40::NT, C40::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      break;
-    }
-    case 48: {
-      const int v = variant(48);
-      if (v == 11) k_tsqr_la<L48, SegDev><<<grid, L48::NT, L48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 12) k_tsqr_la<L48b, SegDev><<<grid, L48b::NT, L48b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 13) k_tsqr_la<L48t, SegDev><<<grid, L48t::NT, L48t::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else k_tsqr<C48><<<grid, C48::NT, C48::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      break;
-    }
-    case 64: {
-      const int v = variant(64, rows);
-      if (v == 10) k_tsqr_la<L64, SegDev><<<grid, L64::NT, L64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 11) k_tsqr_la<L64b, SegDev><<<grid, L64b::NT, L64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 12) k_tsqr_la<L64c, SegDev><<<grid, L64c::NT, L64c::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 13) k_tsqr_la<L64t, SegDev><<<grid, L64t::NT, L64t::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 14) k_tsqr_la<L64u, SegDev><<<grid, L64u::NT, L64u::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 1) k_tsqr<C64a><<<grid, C64a::NT, C64a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 2) k_tsqr<C64b><<<grid, C64b::NT, C64b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 3) k_tsqr_blk<B64, SegDev><<<grid, B64::NT, B64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 4) k_tsqr_blk<B64s, SegDev><<<grid, B64s::NT, B64s::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else k_tsqr<C64><<<grid, C64::NT, C64::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      break;
-    }
-    default: {
-      const int v = variant(128, rows);
-      if (v == 10) k_tsqr_la<L128, SegDev><<<grid, L128::NT, L128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 11) k_tsqr_la<L128b, SegDev><<<grid, L128b::NT, L128b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 13) k_tsqr_la<L128t, SegDev><<<grid, L128t::NT, L128t::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 14) k_tsqr_la<L128u, SegDev><<<grid, L128u::NT, L128u::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 1) k_tsqr<C128a><<<grid, C128a::NT, C128a::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else if (v == 2) k_tsqr<C128b><<<grid, C128b::NT, C128b::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      else k_tsqr<C128><<<grid, C128::NT, C128::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
-      break;
-    }
-  }
+  with_kernel(W, variant(W, rows), [&](auto cfg) {
+    using C = decltype(cfg);
+    if constexpr (IsWarp<C>::value)
+      k_tsqr_warp<C><<<grid, C::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+    else if constexpr (IsLa<C>::value)
+      k_tsqr_la<C, SegDev><<<grid, C::NT, C::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+    else
+      k_tsqr<C><<<grid, C::NT, C::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
+    return 0;
+  });
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
 }

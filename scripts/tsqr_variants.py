@@ -1,4 +1,5 @@
-"""Checks and times TSQR kernel variants against each other and numpy.
+"""Checks and times TSQR kernel variants against each other and numpy
+(variants per width: warp | warpc | cta | lab | lat, see tsqr.cu variant()).
 
 python scripts/tsqr_variants.py W ROWS VAR[,VAR...] [reps]
 Env var FG_TSQR_W<W> selects the variant ('' = default).  Prints time, TF/s
