@@ -304,7 +304,9 @@ __global__ void k_normalize(const double* __restrict__ Rw, int W, int n,
 
 using W4 = WCfg<4, 1, 8, 2>;
 using W8 = WCfg<8, 2, 8, 2>;
+using W8c = WCfg<8, 2, 12, 2>;   // 96-row tiles (measured best at W = 8)
 using W12 = WCfg<12, 3, 8, 2>;
+using W12c = WCfg<12, 3, 12, 2>;  // 96-row tiles (measured best at W = 12)
 using W16 = WCfg<16, 2, 8, 2>;
 using W16c = WCfg<16, 4, 8, 2>;
 using W20 = WCfg<20, 5, 8, 1>;
@@ -394,8 +396,8 @@ template <class F>
 auto with_kernel(int W, Kern k, F&& f) {
   switch (W) {
     case 4: return f(W4{});
-    case 8: return f(W8{});
-    case 12: return f(W12{});
+    case 8: return k == Kern::WarpC ? f(W8{}) : f(W8c{});
+    case 12: return k == Kern::WarpC ? f(W12{}) : f(W12c{});
     case 16: return k == Kern::Cta ? f(C16{}) : k == Kern::Warp ? f(W16{}) : f(W16c{});
     case 20: return f(W20{});
     case 24: return f(W24{});
