@@ -310,6 +310,7 @@ using W12c = WCfg<12, 3, 12, 2>;  // 96-row tiles (measured best at W = 12)
 using W16 = WCfg<16, 2, 8, 2>;
 using W16c = WCfg<16, 4, 8, 2>;
 using W20 = WCfg<20, 5, 8, 1>;
+using W20t = WCfg<20, 5, 14, 1>;  // 112-row tiles (measured best at W = 20)
 using W24 = WCfg<24, 3, 8, 2>;
 using W32c = WCfg<32, 4, 8, 2>;
 using C16 = Cfg<16, 8, 16, 16>;
@@ -399,7 +400,7 @@ auto with_kernel(int W, Kern k, F&& f) {
     case 8: return k == Kern::WarpC ? f(W8{}) : f(W8c{});
     case 12: return k == Kern::WarpC ? f(W12{}) : f(W12c{});
     case 16: return k == Kern::Cta ? f(C16{}) : k == Kern::Warp ? f(W16{}) : f(W16c{});
-    case 20: return f(W20{});
+    case 20: return k == Kern::WarpC ? f(W20{}) : f(W20t{});
     case 24: return f(W24{});
     case 32: return k == Kern::Cta ? f(C32{}) : (k == Kern::Warp || k == Kern::WarpC) ? f(W32c{}) : f(L32{});
     case 40: return k == Kern::Cta ? f(C40{}) : f(L40{});
