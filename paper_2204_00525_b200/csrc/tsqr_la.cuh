@@ -6,14 +6,20 @@
 // the transformation is the structured Householder QR of [R; X] (LAPACK
 // tpqrt: reflector k touches row k of R and the B tile rows), as in tsqr.cu.
 //
-// Schedule per B-row tile (X, shared memory, double-buffered: the next tile
-// is staged with cp.async while this one is factored):
+// Schedule per B-row tile (X in shared memory):
+//   stage the tile (cp.async; 16-byte copies when it lies inside one dense
+//   segment; NBUF = 2 stages the next tile while this one is factored);
 //   warp 0 factors panel 0;                                         barrier
 //   for p = 0 .. NP-1:
 //     warp 0     : block p+1 -= panel p (DMMA), then factors panel p+1
 //     warps 1..  : blocks p+2 .. NP-1 -= panel p (DMMA)            barrier
 // so the serial panel chain overlaps the tensor-core work of the previous
-// panel instead of leaving seven warps at a barrier.
+// panel instead of leaving the other warps at a barrier.  A panel whose tile
+// columns are exactly zero (stacked triangular factors in merge levels) is
+// the identity and is skipped together with the block updates it drives.
+// The default configurations (tsqr.cu) are single-buffered with 64-row
+// tiles; for large spans R is kept as upper-triangular 8 x 8 blocks (RTRI)
+// so that 2-warp CTAs fit 4 per SM at W = 64.
 //
 // Panel (warp 0): lane (g, t) = (lane / 4, lane % 4) owns panel column g
 // and tile rows 4i + t (the "quad" layout; the same registers are the A
