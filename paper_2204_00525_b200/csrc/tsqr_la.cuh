@@ -33,7 +33,8 @@
 // repaired after the next reduction (warp-uniform, rare).
 // Reflectors are H_k = I - s_k^2 u u^T, u = [alpha - beta; x]; the block
 // reflector uses u~ = s_k u so that H_0 ... H_7 = I - U~ T U~^T, unit-diagonal
-// T (T[g][k] = -sum_j T[g][j] G~[j][k], G~ = U~^T U~).
+// T (T[g][k] = -sum_j T[g][j] G~[j][k], G~ = U~^T U~), built inside the
+// column loop from the same reductions.
 //
 // Trailing block J against panel P (one warp):
 //   Y = U~^T [R_PJ; X_J]  (DMMA, K = tile rows),  W' = T^T Y,
@@ -65,7 +66,7 @@ struct LCfg {
   static_assert(NBUF == 1 || NBUF == 2, "buffers");
   static constexpr size_t r_doubles = RTRI ? (size_t)NP * (NP + 1) / 2 * 64 : (size_t)W * LDR;
   static constexpr size_t smem_doubles =
-      r_doubles + NBUF * (size_t)B * LDX + 2 * 64 + 2 * 8 + 64 + 64 * WARPS;
+      r_doubles + NBUF * (size_t)B * LDX + 2 * 64 + 2 * 8 + 64 * WARPS;
   static constexpr size_t smem_bytes = smem_doubles * 8 + B * sizeof(int);
 };
 
@@ -194,8 +195,7 @@ __device__ __forceinline__ void dm_trailing(double* __restrict__ X, double* __re
 template <class C>
 __device__ __forceinline__ bool la_panel(double* __restrict__ X, double* __restrict__ R,
                                          int p0, double* __restrict__ Ts,
-                                         double* __restrict__ ut, double* __restrict__ Gs,
-                                         int lane) {
+                                         double* __restrict__ ut, int lane) {
   constexpr int RPL = C::RPL;
   const int g = lane >> 2, t = lane & 3;
   double Xp[RPL];
@@ -221,7 +221,12 @@ __device__ __forceinline__ bool la_panel(double* __restrict__ X, double* __restr
   double al = __shfl_sync(0xffffffffu, Rd[0], 0);
   SRefl h = srefl_fast(al, sk);
   bool redo_norm = false, redo_refl = !srefl_ok(al, sk);
-  double Gk[8];  // s_k * v_g . v_k (X parts) for k > g
+  // Row g of T, built column by column: T[g][k] = -sum_{j<k} T[g][j] G~[j][k]
+  // with G~[j][k] = s_j s_k v_j . v_k (the X parts; u~'s R parts are on
+  // different rows), gathered from the quads' reductions of step k.
+  double Tr[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) Tr[k] = k == g ? 1.0 : 0.0;
   double my_s = 0.0, my_u = 0.0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -258,7 +263,13 @@ __device__ __forceinline__ bool la_panel(double* __restrict__ X, double* __restr
       sig = fma(f, fma(f, sk, -2.0 * dot), sig);
       smax = fmax(smax, sig);
     }
-    Gk[k] = dot * h.s;
+    if (k > 0) {
+      const double gt = dot * h.s * my_s;  // G~[g][k], valid for g < k
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < k; ++j) acc = fma(Tr[j], __shfl_sync(0xffffffffu, gt, 4 * j), acc);
+      if (g < k) Tr[k] = -acc;
+    }
     if (g == k) {
       my_s = h.s;
       my_u = h.u0 * h.s;
@@ -277,19 +288,7 @@ __device__ __forceinline__ bool la_panel(double* __restrict__ X, double* __restr
 #pragma unroll
   for (int i = 0; i < 8; ++i)
     if ((i & 3) == t) rblock<C>(R, p0 / 8, p0 / 8)[i * rld<C>() + g] = Rd[i];
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if ((k & 3) == t) Gs[g * 8 + k] = k > g ? Gk[k] * my_s : 0.0;
   if (t == 0) ut[g] = my_u;
-  __syncwarp();
-  double Tr[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < k; ++j) acc = fma(Tr[j], Gs[j * 8 + k], acc);
-    Tr[k] = k < g ? 0.0 : (k == g ? 1.0 : -acc);
-  }
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     if ((k & 3) == t) Ts[g * 8 + k] = Tr[k];
@@ -308,9 +307,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   double* Xb1 = Xb0 + (C::NBUF - 1) * C::B * C::LDX;
   double* Tsb = Xb1 + C::B * C::LDX;             // 2 x (8 x 8), by panel parity
   double* utb = Tsb + 128;                       // 2 x 8
-  double* Gs = utb + 16;                         // 8 x 8 (warp 0)
   __shared__ int zpan[2];                        // panel of parity pb is the identity
-  double* scr = Gs + 64;                         // 64 per warp
+  double* scr = utb + 16;                        // 64 per warp
   int* rowseg = reinterpret_cast<int*>(scr + 64 * C::WARPS);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -329,7 +327,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     if (C::NBUF == 2 && tt + nunits < total_tiles)
       la_stage<C>(segs, nseg, total_rows, tt + nunits, buf ? Xb0 : Xb1, rowseg);
     if (warp == 0) {
-      const bool z = la_panel<C>(X, R, 0, Tsb, utb, Gs, lane);
+      const bool z = la_panel<C>(X, R, 0, Tsb, utb, lane);
       if (lane == 0) zpan[0] = z;
     }
     __syncthreads();
@@ -342,7 +340,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         if (p + 1 < NP) {
           if (!zp) dm_trailing<C>(X, R, 8 * p, 8 * (p + 1), Tp, up, my, lane);
           const bool z = la_panel<C>(X, R, 8 * (p + 1), Tsb + 64 * (pb ^ 1), utb + 8 * (pb ^ 1),
-                                     Gs, lane);
+                                     lane);
           if (lane == 0) zpan[pb ^ 1] = z;
         }
       } else if (!zp) {
