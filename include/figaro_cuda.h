@@ -115,6 +115,18 @@ typedef struct fg_result {
                           /* fused heads/tails->TSQR) kernels of the call  */
   double seconds_tsqr_kernels;     /* device time of the TSQR stage        */
   int64_t headtail_launches;
+  /* Algorithmic units of the timed launches (SURVEY
+   * 8(d)): bytes = 8 x (input data elements read + summary elements read
+   * + head/summary elements written + tail elements written to HBM) of the
+   * heads/tails launches; flops = 2 m w^2 - 2/3 w^3 per column span, split
+   * between the spans absorbed inside the fused heads/tails kernels and the
+   * spans (plus the 2/3 N^3 final merge) factored in the TSQR stage.     */
+  double headtail_bytes;
+  double headtail_fused_flops;
+  double tsqr_stage_flops;
+  int64_t fused_launches;         /* heads/tails launches that were fused  */
+  int64_t host_syncs;             /* host<->device synchronisations       */
+  int64_t reserved[3];
 } fg_result;
 
 /* Runs validate_join_tree, counts, the FiGaRo transform and the TSQR

@@ -50,7 +50,10 @@ class fg_result(C.Structure):
                 ("seconds_postprocess", C.c_double),
                 ("seconds_total", C.c_double), ("kernels", C.c_int64),
                 ("seconds_headtail_kernels", C.c_double),
-                ("seconds_tsqr_kernels", C.c_double), ("headtail_launches", C.c_int64)]
+                ("seconds_tsqr_kernels", C.c_double), ("headtail_launches", C.c_int64),
+                ("headtail_bytes", C.c_double), ("headtail_fused_flops", C.c_double),
+                ("tsqr_stage_flops", C.c_double), ("fused_launches", C.c_int64),
+                ("host_syncs", C.c_int64), ("reserved", C.c_int64 * 3)]
 
 
 class fg_block(C.Structure):

@@ -176,6 +176,7 @@ struct Context {
   size_t smem_optin = 0;
   std::string last_error = "ok";
   int64_t launches = 0;
+  int64_t syncs = 0;          // host waits on the context stream
   BlockCache cache;           // declared before every DevArray member
   DevArray<unsigned> status;  // device status word
   // Results of the last pipeline run, kept for fg_get_* inspection.
@@ -184,6 +185,12 @@ struct Context {
 };
 
 #define FG_LAUNCHED(ctx) (++(ctx).launches)
+
+// The one way the library waits for its stream (counted in fg_result).
+inline void sync_stream(Context& ctx) {
+  ++ctx.syncs;
+  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+}
 #define FG_KERNEL_CHECK() FG_CUDA(cudaPeekAtLastError())
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -427,7 +427,7 @@ void group_sorted_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
   int64_t G = 0;
   FG_CUDA(cudaMemcpyAsync(&G, pend.nr.get(), sizeof G, cudaMemcpyDeviceToHost,
                           ctx.stream));
-  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  sync_stream(ctx);
   group_finish(ctx, G, out, pend);
 }
 

@@ -230,7 +230,7 @@ std::vector<AttrCode> encode_attributes(Context& ctx,
                             cudaMemcpyDeviceToHost, st));
     FG_CUDA(cudaMemcpyAsync(hmax.data(), dmax.get(), dmax.bytes(),
                             cudaMemcpyDeviceToHost, st));
-    FG_CUDA(cudaStreamSynchronize(st));
+    sync_stream(ctx);
     for (int a = 0; a < n_attr; ++a) {
       if (hmin[a] > hmax[a]) { code[a] = {0, 0}; continue; }  // no rows
       code[a].min = hmin[a];

@@ -193,7 +193,7 @@ void semi_join(Context& ctx, NodeState& a, NodeState& b,
   int64_t m = 0;
   FG_CUDA(cudaMemcpyAsync(&m, nsel.get(), sizeof m, cudaMemcpyDeviceToHost,
                           ctx.stream));
-  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  sync_stream(ctx);
   a.sel = std::move(next);
   a.has_sel = true;
   a.rows = m;
@@ -211,7 +211,7 @@ void check_status(Context& ctx, const char* phase) {
   unsigned st = 0;
   FG_CUDA(cudaMemcpyAsync(&st, ctx.status.get(), sizeof st,
                           cudaMemcpyDeviceToHost, ctx.stream));
-  FG_CUDA(cudaStreamSynchronize(ctx.stream));
+  sync_stream(ctx);
   if (!st) return;
   const std::string p = phase;
   if (st & ST_MISSING_CHILD)
@@ -345,6 +345,13 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   Trace tr;
   Events ev;
   KernelTimer kt_ht(st), kt_tsqr(st);
+  // Algorithmic units of the timed launches.
+  double ht_bytes = 0, fused_flops = 0, tsqr_flops = 0;
+  int64_t fused_launches = 0;
+  const int64_t syncs0 = ctx.syncs;
+  auto span_flops = [](double m, double w) {
+    return m > 0 && w > 0 ? 2.0 * m * w * w - 2.0 / 3.0 * w * w * w : 0.0;
+  };
   FG_CUDA(cudaEventRecord(ev.e[0], st));
 
   // Inputs on the device.  Host inputs are uploaded on the context's copy
@@ -456,7 +463,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     for (size_t ni = 0; ni < nodes.size(); ++ni)
       FG_CUDA(cudaMemcpyAsync(&Gs[ni], pend[ni].nr.get(), sizeof(int64_t),
                               cudaMemcpyDeviceToHost, st));
-    FG_CUDA(cudaStreamSynchronize(st));
+    sync_stream(ctx);
     for (size_t ni = 0; ni < nodes.size(); ++ni) {
       NodeState& n = *nodes[ni];
       group_finish(ctx, Gs[ni], n.grp, pend[ni]);
@@ -511,7 +518,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
                                 cudaMemcpyDeviceToHost, st));
         any = true;
       }
-    if (any) FG_CUDA(cudaStreamSynchronize(st));
+    if (any) sync_stream(ctx);
     for (size_t ni = 0; ni < nodes.size(); ++ni) {
       NodeState& n = *nodes[ni];
       if (n.parent < 0) continue;
@@ -647,6 +654,14 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       run_heads_tails(ctx, a);
     }
     kt_ht.end();
+    // input elements read once + heads written once (+ tails written once
+    // when they go to HBM; fused tails stay on chip)
+    ht_bytes += 8.0 * ((double)n.rows * n.w + (double)G * n.w +
+                       (n.fused_count ? 0.0 : (double)n_tails * n.w));
+    if (n.fused_count) {
+      ++fused_launches;
+      fused_flops += span_flops((double)n_tails, n.w);
+    }
     if (!is_leaf) {
       JoinArgs j{};
       j.G = G;
@@ -702,6 +717,10 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
         kt_ht.begin();
         run_heads_tails(ctx, b);
         kt_ht.end();
+        // summary rows read once, parent-key heads and projection tails
+        // written once
+        ht_bytes += 8.0 * ((double)G * n.width + (double)n.P * n.width +
+                           (double)(G - n.P) * n.width);
       }
       n.sum_S = n.Sq.get();
       n.sum_scale = n.scale_q.get();
@@ -750,9 +769,11 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
         sp.W = sn.pfused_W;
       }
     }
+    if (!sp.partials) tsqr_flops += span_flops((double)s.rows, (double)s.cols);
     tsq.push_back(sp);
   }
   const int N = (int)lay.total;
+  tsqr_flops += 2.0 / 3.0 * (double)N * N * N;  // final merge of span factors
   DevArray<double> Rdev;
   double* Rd = R_out;
   if (opt.memory == FG_MEM_HOST) {
@@ -767,7 +788,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   if (opt.memory == FG_MEM_HOST && N > 0)
     FG_CUDA(cudaMemcpyAsync(R_out, Rd, sizeof(double) * N * N,
                             cudaMemcpyDeviceToHost, st));
-  FG_CUDA(cudaStreamSynchronize(st));
+  sync_stream(ctx);
   FG_CUDA(cudaGetLastError());
   tr.mark("final sync");
 
@@ -786,6 +807,11 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     res->seconds_headtail_kernels = kt_ht.seconds();
     res->seconds_tsqr_kernels = kt_tsqr.seconds();
     res->headtail_launches = (int64_t)kt_ht.ev.size();
+    res->headtail_bytes = ht_bytes;
+    res->headtail_fused_flops = fused_flops;
+    res->tsqr_stage_flops = tsqr_flops;
+    res->fused_launches = fused_launches;
+    res->host_syncs = ctx.syncs - syncs0;
   }
   // Keep the inspection state; drop the bulky buffers unless R0 is wanted.
   saved->have_r0 = opt.keep_r0 != 0;
@@ -1003,7 +1029,7 @@ fg_status fg_get_keys(fg_ctx* c, int32_t node, int32_t parent_keys,
                       d.get());
     FG_CUDA(cudaMemcpyAsync(out, d.get(), d.bytes(), cudaMemcpyDeviceToHost,
                             ctx.stream));
-    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+    sync_stream(ctx);
   });
 }
 
@@ -1086,7 +1112,7 @@ fg_status fg_group_keys(fg_ctx* c, const uint64_t* keys, int64_t n,
     if (g.G)
       FG_CUDA(cudaMemcpyAsync(uniq, g.uniq.get(), g.G * sizeof(uint64_t),
                               cudaMemcpyDeviceToDevice, ctx.stream));
-    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+    sync_stream(ctx);
     *G = g.G;
   });
 }
@@ -1120,7 +1146,7 @@ fg_status fg_heads_tails(fg_ctx* c, const double* data, int64_t ld, int32_t w,
     a.ldt = ldt;
     a.scales = scales;
     fg::run_heads_tails(ctx, a);
-    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+    sync_stream(ctx);
   });
 }
 
@@ -1136,7 +1162,7 @@ fg_status fg_tsqr(fg_ctx* c, int32_t n_blocks, const fg_block* blocks,
       spans.push_back({b.data, b.rows, b.ld, b.cols, b.col_begin});
     }
     fg::tsqr(ctx, spans, n, R_out);
-    FG_CUDA(cudaStreamSynchronize(ctx.stream));
+    sync_stream(ctx);
   });
 }
 

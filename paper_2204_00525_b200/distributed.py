@@ -88,3 +88,28 @@ def device_merge(parts, n: int, device: int = 0):
     """Merge on the GPU: TSQR of the stacked factors (fg_tsqr)."""
     from .figaro import tsqr
     return tsqr([(p, 0) for p in parts], n, device=device)
+
+
+def weak_shard(db, rank: int, world: int):
+    """Weak scaling: rank r's database is a full-size config generated with
+    its own seed whose key values are moved to hash bucket r's key range
+    (v -> v * world + r for every key column), so the P databases are the
+    key-hash shards of one P-times larger database."""
+    if world > 1:
+        for r in db.relations:
+            if r.keys.size:
+                r.keys = r.keys * world + rank
+    return db
+
+
+def shard_database(db, rank: int, world: int):
+    """Strong scaling: rank r's shard of ONE global database (fgdb.Database)
+    through the partitioner (shard_relations on partition_attribute)."""
+    from .fgdb import Database, RelationData
+    attr = partition_attribute(db.relations, db.root)
+    rels = shard_relations(db.relations, attr, rank, world,
+                           make=lambda r, k, d: RelationData(r.name, list(r.key_attrs),
+                                                             list(r.data_attrs),
+                                                             np.ascontiguousarray(k),
+                                                             np.ascontiguousarray(d)))
+    return Database(rels, db.root, list(db.parent))

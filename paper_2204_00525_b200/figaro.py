@@ -87,6 +87,7 @@ class Context:
             raise cuda_error(f"fg_ctx_create(device={device}) failed with status {st}: "
                              "needs an sm_100 GPU (no CPU fallback)")
         self.h = h
+        self._bound = None
 
     def check(self, st: int):
         if st != L.FG_OK:
@@ -98,7 +99,21 @@ class Context:
         return self.lib.fg_ctx_stream(self.h) or 0
 
     def set_stream(self, stream_ptr: int):
-        self.check(self.lib.fg_ctx_set_stream(self.h, C.c_void_p(stream_ptr)))
+        """Orders the context's work on `stream_ptr` (a cudaStream_t).  0 is
+        torch's legacy default stream, bound as cudaStreamLegacy -- the C
+        ABI's NULL means "the context's own stream"."""
+        ptr = stream_ptr or _CUDA_STREAM_LEGACY
+        if ptr == self._bound:
+            return
+        self.check(self.lib.fg_ctx_set_stream(self.h, C.c_void_p(ptr)))
+        self._bound = ptr
+
+    def bind_current_stream(self):
+        """Binds the context to torch's current stream on its device, so
+        device tensors produced by torch (or NCCL) are complete before the
+        library reads them and results are ordered before torch's next op."""
+        import torch
+        self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
     def kernel_launches(self) -> int:
         return int(self.lib.fg_kernel_launches(self.h))
@@ -116,6 +131,7 @@ class Context:
 
 
 _contexts: Dict[int, Context] = {}
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream
 
 
 def get_context(device: int = 0) -> Context:
@@ -147,6 +163,9 @@ class Relation:
         for x in (self.keys, self.data):
             if getattr(x, "ndim", 0) == 2:
                 rows = int(x.shape[0])
+        if _is_torch(self.keys) or _is_torch(self.data):
+            self._normalise_torch(rows)
+            return
         if not _is_torch(self.keys):
             k = np.asarray(self.keys, dtype=np.int64)
             self.keys = np.ascontiguousarray(
@@ -155,6 +174,22 @@ class Relation:
             d = np.asarray(self.data, dtype=np.float64)
             self.data = np.ascontiguousarray(
                 d.reshape(rows if rows is not None else -1, len(self.data_attrs)))
+
+    def _normalise_torch(self, rows):
+        """Torch inputs: both tensors must live on one CUDA device; keys
+        become contiguous int64 (rows, n_key), data contiguous float64
+        (rows, n_data) -- the row-major layout the C ABI reads by pointer."""
+        import torch
+        if not (_is_torch(self.keys) and _is_torch(self.data)):
+            raise error(f"relation {self.name}: keys and data must both be torch tensors "
+                        "or both host arrays")
+        if not (self.keys.is_cuda and self.data.is_cuda) or self.keys.device != self.data.device:
+            raise error(f"relation {self.name}: keys and data must be on the same CUDA device")
+        nk, nd = len(self.key_attrs), len(self.data_attrs)
+        if rows is None:
+            rows = int(self.keys.numel() // nk) if nk else int(self.data.numel() // max(nd, 1))
+        self.keys = self.keys.to(torch.int64).reshape(rows, nk).contiguous()
+        self.data = self.data.to(torch.float64).reshape(rows, nd).contiguous()
 
     def row_count(self) -> int:
         return int(self.keys.shape[0])
@@ -318,6 +353,11 @@ class PipelineResult:
     seconds_headtail_kernels: float = 0.0
     seconds_tsqr_kernels: float = 0.0
     headtail_launches: int = 0
+    headtail_bytes: float = 0.0
+    headtail_fused_flops: float = 0.0
+    tsqr_stage_flops: float = 0.0
+    fused_launches: int = 0
+    host_syncs: int = 0
     counts: Optional[List[NodeCounts]] = None
     r0: Optional[List[OutSpan]] = None
 
@@ -372,6 +412,7 @@ def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
     n = layout.total
     if device_mem:
         import torch
+        ctx.bind_current_stream()
         R = torch.empty((n, n), dtype=torch.float64, device=rels[0].data.device)
         rp = R.data_ptr()
     else:
@@ -390,7 +431,9 @@ def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
         seconds_total=res.seconds_total, kernels=res.kernels,
         seconds_headtail_kernels=res.seconds_headtail_kernels,
         seconds_tsqr_kernels=res.seconds_tsqr_kernels,
-        headtail_launches=res.headtail_launches)
+        headtail_launches=res.headtail_launches, headtail_bytes=res.headtail_bytes,
+        headtail_fused_flops=res.headtail_fused_flops, tsqr_stage_flops=res.tsqr_stage_flops,
+        fused_launches=res.fused_launches, host_syncs=res.host_syncs)
     if fetch_counts:
         out.counts = [fetch_node_counts(ctx, i, rels[i], tree) for i in range(len(rels))]
     if keep_r0:
@@ -465,6 +508,8 @@ def join_size(relations: Sequence[Relation], tree: JoinTree, cap: int = DEFAULT_
     ctx = get_context(device)
     rels = list(relations)
     arr, keep, device_mem = _marshal(rels, "join_size")
+    if device_mem:
+        ctx.bind_current_stream()
     parent = (C.c_int32 * len(rels))(*tree.parent)
     rows = C.c_int64()
     ctx.check(ctx.lib.fg_join_size(ctx.h, len(rels), arr, tree.root, parent,
@@ -492,6 +537,8 @@ def materialize_join(relations: Sequence[Relation], tree: JoinTree,
     n = make_layout(rels, tree).total
     rows = join_size(rels, tree, cap, device)
     arr, keep, device_mem = _marshal(rels, "materialize_join")
+    if device_mem:
+        ctx.bind_current_stream()
     A, ap = _out(rows, n, device_mem, rels[0].data if rels else None)
     if rows and n:
         parent = (C.c_int32 * len(rels))(*tree.parent)
@@ -515,7 +562,9 @@ def recover_q(relations: Sequence[Relation], tree: JoinTree, R, cap: int = DEFAU
     n = make_layout(rels, tree).total
     arr, keep, device_mem = _marshal(rels, "recover_q")
     if device_mem:
-        Rc = R.contiguous()
+        import torch
+        ctx.bind_current_stream()
+        Rc = R.to(torch.float64).contiguous()
         rp = Rc.data_ptr()
     else:
         Rc = np.ascontiguousarray(np.asarray(R, dtype=np.float64))
@@ -551,6 +600,8 @@ def group_keys(keys, bits: int, device: int = 0):
     Returns (perm int32, begins int32 [G+1], uniq int64 [G])."""
     import torch
     ctx = get_context(device)
+    ctx.bind_current_stream()
+    keys = keys.contiguous()
     n = keys.numel()
     perm = torch.empty(n, dtype=torch.int32, device=keys.device)
     begins = torch.empty(n + 1, dtype=torch.int32, device=keys.device)
@@ -566,6 +617,9 @@ def heads_tails(data, begins, perm=None, weights=None, tail_count=None, device: 
     Returns (heads (G, w), tails (rows-G, w), scales (G,))."""
     import torch
     ctx = get_context(device)
+    ctx.bind_current_stream()
+    if data.dtype != torch.float64 or data.stride(1) != 1:
+        raise error("heads_tails: data must be float64 with contiguous rows")
     rows, w = data.shape
     G = begins.numel() - 1
     heads = torch.zeros((max(G, 0), w), dtype=torch.float64, device=data.device)
@@ -582,9 +636,15 @@ def tsqr(blocks, n: int, device: int = 0):
     """K6/K7: sign-normalised n x n R of stacked blocks [(tensor, col_begin)]."""
     import torch
     ctx = get_context(device)
+    ctx.bind_current_stream()
     arr = (L.fg_block * max(1, len(blocks)))()
     for i, (t, cb) in enumerate(blocks):
-        arr[i] = L.fg_block(t.data_ptr(), t.shape[0], t.stride(0), t.shape[1], cb)
+        if t.dtype != torch.float64 or not t.is_cuda or t.dim() != 2:
+            raise error("tsqr: blocks must be 2-D float64 CUDA tensors")
+        if t.shape[0] > 1 and t.shape[1] > 1 and t.stride(1) != 1:
+            raise error("tsqr: block rows must be contiguous (stride(1) == 1)")
+        arr[i] = L.fg_block(t.data_ptr(), t.shape[0], max(t.stride(0), t.shape[1]),
+                            t.shape[1], cb)
     dev = blocks[0][0].device if blocks else torch.device("cuda", device)
     R = torch.empty((n, n), dtype=torch.float64, device=dev)
     ctx.check(ctx.lib.fg_tsqr(ctx.h, len(blocks), arr, n, R.data_ptr()))
