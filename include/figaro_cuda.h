@@ -52,7 +52,8 @@ enum {
   FG_E_EMPTY_JOIN = 6,  /* figaro::empty_join_error                       */
   FG_E_UNSUPPORTED = 7, /* input shape this build does not handle         */
   FG_E_CUDA = 8,        /* CUDA runtime / launch failure                  */
-  FG_E_RANK = 9         /* figaro::rank_error (singular R in recover_q)   */
+  FG_E_RANK = 9,        /* figaro::rank_error (singular R in recover_q)   */
+  FG_E_NCCL = 10        /* NCCL failure in fg_gather_r                    */
 };
 
 typedef struct fg_ctx fg_ctx;
@@ -243,6 +244,19 @@ FG_API fg_status fg_recover_q(fg_ctx* ctx, int32_t n_rel, const fg_relation* rel
                               int32_t root, const int32_t* parent, int32_t memory,
                               uint64_t cap, const double* R, double* A_out,
                               double* Q_out, int64_t* rows);
+
+/* ---- multi-GPU ------------------------------------------- */
+
+/* One process (or host thread) per GPU, one context each.  Attach the rank's
+ * NCCL communicator (an ncclComm_t passed as void*; NULL detaches).  NCCL is
+ * resolved from the calling process at run time. */
+FG_API fg_status fg_ctx_set_nccl(fg_ctx* ctx, void* nccl_comm);
+/* All-gathers every rank's n x n factor R_local (row-major; device or host
+ * per `memory`) over the communicator and writes the merged, sign-normalised
+ * global R (one more TSQR of the P stacked factors) to R_out.  Every rank
+ * calls it collectively with the same n; every rank gets the same R. */
+FG_API fg_status fg_gather_r(fg_ctx* ctx, const double* R_local, int32_t n,
+                             int32_t memory, double* R_out);
 
 #ifdef __cplusplus
 }

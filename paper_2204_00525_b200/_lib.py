@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("FG_LIB") or os.path.join(_HERE, "lib", "libfigaro_cud
 
 FG_OK = 0
 FG_E_ARG, FG_E_SCHEMA, FG_E_TREE, FG_E_INTEGRITY, FG_E_SIZE = 1, 2, 3, 4, 5
-FG_E_EMPTY_JOIN, FG_E_UNSUPPORTED, FG_E_CUDA, FG_E_RANK = 6, 7, 8, 9
+FG_E_EMPTY_JOIN, FG_E_UNSUPPORTED, FG_E_CUDA, FG_E_RANK, FG_E_NCCL = 6, 7, 8, 9, 10
 FG_MEM_DEVICE, FG_MEM_HOST = 0, 1
 FG_ENGINE_THIN, FG_ENGINE_HOUSEHOLDER = 0, 1
 (FG_ROWS_PER_KEY, FG_THETA_DOWN, FG_FULL_JOIN_SIZE, FG_PHI_CIRC,
@@ -26,7 +26,8 @@ EXPORTED = [
     "fg_run_pipeline", "fg_get_sizes", "fg_get_segments", "fg_get_keys",
     "fg_get_counts", "fg_get_permutation", "fg_get_r0_span_count",
     "fg_get_r0_span", "fg_group_keys", "fg_heads_tails", "fg_tsqr",
-    "fg_join_size", "fg_materialize_join", "fg_recover_q",
+    "fg_join_size", "fg_materialize_join", "fg_recover_q", "fg_ctx_set_nccl",
+    "fg_gather_r",
 ]
 
 
@@ -106,6 +107,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
             "fg_materialize_join": (I32, [P, I32, C.POINTER(fg_relation), I32,
                                           C.POINTER(I32), I32, C.c_uint64, P,
                                           C.POINTER(I64)]),
+            "fg_ctx_set_nccl": (I32, [P, P]),
+            "fg_gather_r": (I32, [P, P, I32, I32, P]),
             "fg_recover_q": (I32, [P, I32, C.POINTER(fg_relation), I32, C.POINTER(I32),
                                    I32, C.c_uint64, P, P, P, C.POINTER(I64)]),
         }

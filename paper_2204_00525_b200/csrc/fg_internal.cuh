@@ -169,14 +169,15 @@ struct NodeState;
 
 struct Context {
   int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = true;
+  cudaStream_t stream = nullptr;  // where all work of the context is ordered
+  cudaStream_t own = nullptr;     // the context's own stream (fg_ctx_create)
   cudaStream_t copy_stream = nullptr;  // host -> device uploads (run_pipeline)
   int sm_count = 148;
   size_t smem_optin = 0;
   std::string last_error = "ok";
   int64_t launches = 0;
   int64_t syncs = 0;          // host waits on the context stream
+  void* nccl = nullptr;       // ncclComm_t of this rank (fg_ctx_set_nccl)
   BlockCache cache;           // declared before every DevArray member
   DevArray<unsigned> status;  // device status word
   // Results of the last pipeline run, kept for fg_get_* inspection.

@@ -177,6 +177,11 @@ struct Span {
 // R (n x n, row-major, device) of the stacked spans, sign-normalised.
 void tsqr(Context& ctx, const std::vector<Span>& spans, int n, double* R_out);
 
+// ---- gather.cu -------------------------------------------------------------
+void set_nccl(Context& ctx, void* comm);
+// All-gather of the ranks' n x n factors + device TSQR merge (syncs).
+void gather_r(Context& ctx, const double* R_local, int n, int memory, double* R_out);
+
 // ---- join.cu ---------------------------------------------------------------
 // Join rows in for_each_join_row order; count only when A_out and Q_out are
 // null; Q = A R^-1 when Q_out is set (R host or device per `memory`).

@@ -395,7 +395,9 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     FG_CUDA(cudaStreamWaitEvent(st, up.keys, 0));
   }
   FG_CUDA(cudaEventRecord(ev.e[1], st));
-  ctx.status.zero();
+  // The status word outlives streams bound with fg_ctx_set_stream: clear it
+  // on the stream this call runs on.
+  FG_CUDA(cudaMemsetAsync(ctx.status.get(), 0, sizeof(unsigned), st));
   tr.mark("setup+upload");
 
   // ---- attribute encodings (global, per attribute name)
@@ -910,7 +912,8 @@ fg_status fg_ctx_create(int32_t device, fg_ctx** out) {
     }
     ctx->sm_count = prop.multiProcessorCount;
     ctx->smem_optin = prop.sharedMemPerBlockOptin;
-    FG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    FG_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+    ctx->stream = ctx->own;
     FG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     // Keep freed pool memory: no OS round trips in steady state.
     cudaMemPool_t pool;
@@ -941,7 +944,10 @@ fg_status fg_ctx_destroy(fg_ctx* c) {
   ctx->status.release();
   ctx->cache.trim();
   fg::current_cache() = nullptr;
-  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->own) {
+    cudaStreamSynchronize(ctx->own);
+    cudaStreamDestroy(ctx->own);
+  }
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -953,15 +959,10 @@ fg_status fg_ctx_destroy(fg_ctx* c) {
 fg_status fg_ctx_set_stream(fg_ctx* c, void* s) {
   return fg::guard(c, [&] {
     Context* ctx = reinterpret_cast<Context*>(c);
+    // Work already queued on the old stream completes before the switch;
+    // the context's own stream lives until fg_ctx_destroy.
     FG_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
-    if (s) {
-      ctx->stream = static_cast<cudaStream_t>(s);
-      ctx->own_stream = false;
-    } else {
-      FG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-      ctx->own_stream = true;
-    }
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
   });
 }
 
@@ -1193,6 +1194,18 @@ fg_status fg_recover_q(fg_ctx* c, int32_t n_rel, const fg_relation* rels,
     if (!R) fail(FG_E_ARG, "recover_q: R is null");
     fg::join_rows(*reinterpret_cast<Context*>(c), n_rel, rels, root, parent, memory,
                   cap, R, A_out, Q_out, rows);
+  });
+}
+
+fg_status fg_ctx_set_nccl(fg_ctx* c, void* comm) {
+  return fg::guard(c, [&] { fg::set_nccl(*reinterpret_cast<Context*>(c), comm); });
+}
+
+fg_status fg_gather_r(fg_ctx* c, const double* R_local, int32_t n, int32_t memory,
+                      double* R_out) {
+  return fg::guard(c, [&] {
+    if (!R_local || !R_out) fail(FG_E_ARG, "fg_gather_r: null buffer");
+    fg::gather_r(*reinterpret_cast<Context*>(c), R_local, n, memory, R_out);
   });
 }
 

@@ -62,12 +62,46 @@ int main() {
     figaro::PipelineOptions opts;
     opts.assume_reduced = true;
     auto ref = figaro::run_pipeline(db.relations, db.tree, opts);
-    auto got = figaro::gpu::run_pipeline<figaro::Relation, figaro::JoinTree, RefErrors>(
-        dev, db.relations, db.tree, true);
+    auto got = figaro::gpu::run_pipeline<figaro::PipelineResult, RefErrors>(
+        dev, db.relations, db.tree, opts, /*keep_r0=*/seed % 4 == 0);
+    // The whole PipelineResult: counts map by map, column names, sizes.
+    bool same_counts = got.counts.node.size() == ref.counts.node.size();
+    for (std::size_t i = 0; same_counts && i < ref.counts.node.size(); ++i) {
+      const auto& a = got.counts.node[i];
+      const auto& b = ref.counts.node[i];
+      same_counts = a.rows_per_key == b.rows_per_key && a.theta_down == b.theta_down &&
+                    a.full_join_size == b.full_join_size && a.phi_circ == b.phi_circ &&
+                    a.phi_down == b.phi_down && a.phi_up == b.phi_up;
+    }
+    if (!same_counts || got.factor.column_names != ref.factor.column_names ||
+        got.data_columns != ref.data_columns ||
+        got.counts.total_join_size(db.tree.root) != ref.counts.total_join_size(db.tree.root)) {
+      ++bad;
+      std::printf("seed %llu: counts / column names differ\n", (unsigned long long)seed);
+    }
+    if (got.r0) {
+      // Same R0 rows in the same order (blocks are spans of the reference's blocks).
+      figaro::PipelineResult ref0 = figaro::run_pipeline(db.relations, db.tree, opts, true);
+      const figaro::Matrix dg = got.r0->dense(), dr = ref0.r0->dense();
+      double diff = 0, nrm = 0;
+      bool shape = dg.rows() == dr.rows() && dg.cols() == dr.cols();
+      for (std::size_t i = 0; shape && i < dr.rows() * dr.cols(); ++i) {
+        diff = std::max(diff, std::abs(dg.data()[i] - dr.data()[i]));
+        nrm = std::max(nrm, std::abs(dr.data()[i]));
+      }
+      if (!shape || diff > 1e-12 * std::max(1.0, nrm)) {
+        ++bad;
+        std::printf("seed %llu: R0 differs (shape %d, max diff %.3e)\n",
+                    (unsigned long long)seed, (int)shape, diff);
+      }
+    }
     bool full = ref.factor.zero_diagonal_rows.empty();
     for (std::size_t i = 0; i < ref.factor.r.rows() && full; ++i)
       full = std::abs(ref.factor.r(i, i)) > 1e-8 * std::abs(ref.factor.r(0, 0));
-    const double d = rel_dist(got.r, ref.factor.r, !full);
+    const auto& gr = got.factor.r;
+    const double d =
+        rel_dist(std::vector<double>(gr.data(), gr.data() + gr.rows() * gr.cols()),
+                 ref.factor.r, !full);
     // recover_q with the reference's R: identical (a_row, q_row) streams.
     {
       const figaro::Layout layout = figaro::make_layout(db.relations, db.tree);
@@ -117,8 +151,9 @@ int main() {
   db.relations[0].data.resize(db.relations[0].keys.size(), db.relations[0].data.cols());
   bool threw = false;
   try {
-    figaro::gpu::run_pipeline<figaro::Relation, figaro::JoinTree, RefErrors>(
-        dev, db.relations, db.tree, true);
+    figaro::PipelineOptions o;
+    o.assume_reduced = true;
+    figaro::gpu::run_pipeline<figaro::PipelineResult, RefErrors>(dev, db.relations, db.tree, o);
   } catch (const figaro::integrity_error&) {
     threw = true;
   }

@@ -261,3 +261,86 @@ def test_widths_cover_every_kernel_shape(w1, w2, fuse, tmp_path, ref_bin):
     res, R = run_gpu(db, fuse=fuse)
     assert r_distance(R, ref.R) <= R_TOL
     check_counts(res, ref)
+
+
+def _write_csv_db(db, d):
+    """A database as the reference's config + CSV files (join_tree.hpp:370-445)."""
+    names = [r.name for r in db.relations]
+    lines = []
+    for r in db.relations:
+        with open(os.path.join(d, r.name + ".csv"), "w") as f:
+            f.write(",".join(list(r.key_attrs) + list(r.data_attrs)) + "\n")
+            for k, v in zip(r.keys, r.data):
+                f.write(",".join([str(int(x)) for x in k] + ["%.17g" % x for x in v]) + "\n")
+        lines.append(f"relation {r.name} file={r.name}.csv keys={','.join(r.key_attrs)} "
+                     f"data={','.join(r.data_attrs)}")
+
+    def term(i):
+        kids = [c for c, p in enumerate(db.parent) if p == i and c != db.root]
+        return names[i] + ("(" + ",".join(term(c) for c in kids) + ")" if kids else "")
+
+    lines.append("tree " + term(db.root))
+    p = os.path.join(d, "db.cfg")
+    with open(p, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    return p
+
+
+def _read_csv_matrix(p):
+    with open(p) as f:
+        rows = [ln.rstrip("\n").split(",") for ln in f if ln.strip()]
+    return rows[0], np.array([[float(x) for x in r] for r in rows[1:]])
+
+
+@pytest.mark.parametrize("case", ["db1", "C1", "C4", "rnd_8"])
+def test_driver_swap(case, tmp_path):
+    """The reference CLI driver (driver.hpp:run) with its run_pipeline call
+    swapped for figaro::gpu::run_pipeline<PipelineResult> (INTEGRATION.md;
+    oracle/_ref/driver_swap) against the unmodified driver (driver_ref) on
+    the same config: R, the count dump (write_counts_csv, every map of every
+    node, text-identical), the R0 dump and the Q output."""
+    ref = os.path.join(os.path.dirname(REF_BIN), "driver_ref")
+    swap = os.path.join(os.path.dirname(REF_BIN), "driver_swap")
+    if not (os.path.exists(ref) and os.path.exists(swap)):
+        pytest.skip("driver_ref / driver_swap not built")
+    if case == "db1":
+        cfg = os.path.join(os.path.dirname(__file__), "golden", "csv", "db1.cfg")
+    elif case.startswith("rnd"):
+        cfg = _write_csv_db(fgdb.read_fgdb(golden(case + ".fgdb")), str(tmp_path))
+    else:
+        cfg = _write_csv_db(workloads.make(case, seed=11, scale=0.01), str(tmp_path))
+    outs = {}
+    for tag, exe in (("ref", ref), ("gpu", swap)):
+        o = {k: str(tmp_path / f"{tag}.{k}") for k in ("r", "counts", "r0", "q")}
+        p = subprocess.run([exe, cfg, o["r"], "--counts", o["counts"], "--r0", o["r0"],
+                            "--q", o["q"]], capture_output=True, text=True, timeout=600)
+        outs[tag] = (o, p.stdout, p.returncode, p.stderr)
+    if outs["ref"][2] != 0:  # e.g. rank_error in compute-q: same phase and class
+        assert outs["gpu"][2] == outs["ref"][2], outs["gpu"][3]
+        assert outs["gpu"][3].split(":")[:2] == outs["ref"][3].split(":")[:2]
+        return
+    assert outs["gpu"][2] == 0, outs["gpu"][1] + outs["gpu"][3]
+    outs = {k: v[:2] for k, v in outs.items()}
+    (ro, rlog), (go, glog) = outs["ref"], outs["gpu"]
+    # Log: same relations / M / N / tree / rows(R0) lines (timings differ).
+    keep = lambda s: [ln.split("->")[0] for ln in s.splitlines()  # noqa: E731
+                      if ln.startswith(("relations:", "join tree:", "q rows:"))]
+    assert keep(rlog) == keep(glog)
+    assert [ln.split("rows(R0)=")[1] for ln in rlog.splitlines() if "rows(R0)" in ln] == \
+        [ln.split("rows(R0)=")[1] for ln in glog.splitlines() if "rows(R0)" in ln]
+    with open(ro["counts"]) as a, open(go["counts"]) as b:
+        assert a.read() == b.read()
+    hr, Rr = _read_csv_matrix(ro["r"])
+    hg, Rg = _read_csv_matrix(go["r"])
+    assert hr == hg
+    assert r_distance(Rg, Rr) <= 1e-10
+    h0r, A0r = _read_csv_matrix(ro["r0"])
+    h0g, A0g = _read_csv_matrix(go["r0"])
+    assert h0r == h0g and A0r.shape == A0g.shape
+    assert np.abs(A0r - A0g).max() <= 1e-12 * max(1.0, np.abs(A0r).max())
+    with open(ro["q"]) as a, open(go["q"]) as b:
+        Qr = np.array([[float(x) for x in ln.split(",")] for ln in a if ln.strip()])
+        Qg = np.array([[float(x) for x in ln.split(",")] for ln in b if ln.strip()])
+    assert Qr.shape == Qg.shape
+    if Qr.size:
+        assert np.linalg.norm(Qr - Qg) <= 1e-8 * max(1.0, np.linalg.norm(Qr))
