@@ -22,7 +22,9 @@
 // Short groups (<= kLight rows) re-read those rows (at most kLight, mostly L2
 // hits).  Long groups get it from a deterministic pre-pass: per unit the
 // partial sum of its continuing group, then a per-group scan over units.
-// All results are run-to-run deterministic.
+// All results are run-to-run deterministic: the fused kernel assigns units
+// to warps statically (unit u to warp u mod #warps), so each warp's TSQR
+// accumulator absorbs the same rows in the same order on every run.
 #include <cuda_pipeline.h>
 
 #include <cub/block/block_scan.cuh>
@@ -43,6 +45,8 @@ constexpr int kUnit = 256;           // rows per work unit
 constexpr int kLight = 256;          // groups up to this size recompute carries
 constexpr int kSmemDoubles = 512;    // per-warp row buffer (4 KB)
 constexpr int kMaxRB = 64;           // max rows per batch
+constexpr int kVJMax = 4;            // children of a join-on-read node
+constexpr int kVJRows = 32;          // max rows per batch with join-on-read
 
 struct HtDev {
   const double* data;
@@ -69,10 +73,83 @@ struct HtDev {
                          // cont[u-1] == first group of u
   int* ticket;
   const int* ufirst;     // per unit: group of its first row (or null)
+  // Join-on-read (K4 folded into K5; process_and_join_children,
+  // figaro.hpp:196-230): with nj >= 0 the data row x is never materialised;
+  // it is [jhead[x, :own_w] * all | jS[c][jlidx[c][x]] * f_c ...] with
+  // sc_c = jscale[c][jlidx[c][x]] (0 for a missing child), all = prod_c sc_c,
+  // f_c = weights[x] * prod_{d != c} sc_d, and its weight is weights[x] * all
+  // -- the values and product order of k_join_rows / k_join_elems.
+  int nj;
+  int own_w;
+  const double* jhead;
+  int64_t jld;
+  const int* jlidx[kVJMax];
+  const double* jS[kVJMax];
+  const double* jscale[kVJMax];
+  int jw[kVJMax];
+  int joff[kVJMax];
 };
 
 __device__ __forceinline__ int64_t src_row(const HtDev& a, int64_t p) {
   return a.perm ? (int64_t)a.perm[p] : p;
+}
+
+// Join-on-read factors of summary row x: f[c] for child c's columns, f[nj]
+// for the own columns, idx[c] = child row (-1 missing); returns the weight.
+__device__ __forceinline__ double vj_row(const HtDev& a, int64_t x, double* f, int* idx) {
+  double sc[kVJMax];
+  double all = 1.0;
+#pragma unroll
+  for (int c = 0; c < kVJMax; ++c) {
+    sc[c] = 0.0;
+    idx[c] = -1;
+    if (c < a.nj) {
+      idx[c] = a.jlidx[c][x];
+      sc[c] = idx[c] >= 0 ? a.jscale[c][idx[c]] : 0.0;
+      all *= sc[c];
+    }
+  }
+  const double sk = a.weights[x];
+#pragma unroll
+  for (int c = 0; c < kVJMax; ++c) {
+    if (c >= a.nj) break;
+    double y = sk;
+#pragma unroll
+    for (int d = 0; d < kVJMax; ++d)
+      if (d != c && d < a.nj) y *= sc[d];
+    f[c] = y;
+  }
+  f[a.nj] = all;
+  return sk * all;
+}
+
+// Which block of the joined row column `col` belongs to: child c, or nj
+// for the own columns; `rel` = column within that block.
+__device__ __forceinline__ int vj_span(const HtDev& a, int col, int& rel) {
+  if (col < a.own_w) {
+    rel = col;
+    return a.nj;
+  }
+  int c = 0;
+  while (c + 1 < a.nj && col >= a.joff[c + 1]) ++c;
+  rel = col - a.joff[c];
+  return c;
+}
+
+// VEC adjacent values of joined row x starting at column col (one block).
+template <int VEC>
+__device__ __forceinline__ void vj_load(const HtDev& a, int64_t x, int col, double* out,
+                                        double& wgt) {
+  double f[kVJMax + 1];
+  int idx[kVJMax];
+  wgt = vj_row(a, x, f, idx);
+  int rel = 0;
+  const int c = vj_span(a, col, rel);
+  const double* src = nullptr;
+  if (c == a.nj) src = a.jhead + x * a.jld + rel;
+  else if (idx[c] >= 0) src = a.jS[c] + (int64_t)idx[c] * a.jw[c] + rel;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) out[e] = src ? src[e] * f[c] : 0.0;
 }
 
 // Last group index g with begins[g] <= p, searching g in [lo, hi).
@@ -87,7 +164,7 @@ __device__ __forceinline__ int64_t seg_of(const int* __restrict__ begins,
 
 struct NoFuse {};
 
-template <int CAP>
+template <int CAP, int VJR = 1>
 struct WarpSmemT {
   double buf[CAP];
   double2 coef[kMaxRB];   // {alpha, beta}: tail = a*alpha - S*beta
@@ -96,8 +173,11 @@ struct WarpSmemT {
   int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
   unsigned char startf[kMaxRB];  // 1 where a group starts inside the batch
   const double* rowptr[kMaxRB];
+  double vjf[VJR][kVJMax + 1];   // join-on-read factors per staged row
+  int vjidx[VJR][kVJMax];        // join-on-read child rows per staged row
 };
 using WarpSmem = WarpSmemT<kSmemDoubles>;
+using WarpSmemVJ = WarpSmemT<kSmemDoubles, kVJRows>;
 constexpr int kFusedDoubles = 1280;  // one TSQR tile of tails (B x ls)
 
 __device__ __forceinline__ double fast_rsqrt_d(double q) {
@@ -139,8 +219,14 @@ __device__ __forceinline__ void chunk_colsum(const HtDev& a, int64_t q0, int64_t
 #pragma unroll 8
     for (int t = 0; t < cnt; ++t) {
       const int64_t r = __shfl_sync(0xffffffffu, my_row, t);
-      const double v = weighted ? __shfl_sync(0xffffffffu, my_w, t) : 1.0;
-      if (col >= 0) {
+      double v = weighted ? __shfl_sync(0xffffffffu, my_w, t) : 1.0;
+      if (a.nj >= 0) {
+        double x = 0.0, wv = 1.0;
+        if (col >= 0) vj_load<1>(a, r, col, &x, wv);
+        else { double f[kVJMax + 1]; int idx[kVJMax]; wv = vj_row(a, r, f, idx); }
+        v = wv;
+        if (col >= 0) acc = fma(v, x, acc);
+      } else if (col >= 0) {
         const double x = a.data[r * a.ld + col];
         acc = weighted ? fma(v, x, acc) : acc + x;
       }
@@ -150,10 +236,44 @@ __device__ __forceinline__ void chunk_colsum(const HtDev& a, int64_t q0, int64_t
 }
 
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
-template <int SLOTS, int VEC, class SM>
+template <int SLOTS, int VEC, bool VJ, class SM>
 __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
                                            SM& sm, int64_t p, int nb,
                                            int lane) {
+  if constexpr (VJ) {
+    // Join-on-read: own head columns and child summary rows are copied into
+    // the row buffer; the row factors are applied when the buffer is read.
+    for (int rr = lane; rr < nb; rr += 32) {
+      const int64_t x = src_row(a, p + rr);
+      sm.wt[rr] = vj_row(a, x, sm.vjf[rr], sm.vjidx[rr]);
+      sm.rowptr[rr] = a.jhead + x * a.jld;
+    }
+    __syncwarp();
+    const int g = lane / geo.L, cl = lane % geo.L;
+    for (int rr = g; rr < nb; rr += geo.G) {
+      double* dst = sm.buf + rr * geo.ls;
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s) {
+        const int pk = cl + geo.L * s;
+        if (pk >= geo.np) continue;
+        int rel = 0;
+        const int c = vj_span(a, VEC * pk, rel);
+        if (c == a.nj) {
+          cp_async<VEC>(dst + VEC * pk, sm.rowptr[rr] + rel);
+        } else {
+          const int idx = sm.vjidx[rr][c];
+          if (idx >= 0) {
+            cp_async<VEC>(dst + VEC * pk, a.jS[c] + (int64_t)idx * a.jw[c] + rel);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) dst[VEC * pk + e] = 0.0;
+          }
+        }
+      }
+    }
+    __pipeline_commit();
+    return;
+  }
   for (int rr = lane; rr < nb; rr += 32)
     sm.rowptr[rr] = a.data + src_row(a, p + rr) * a.ld;
   __syncwarp();
@@ -173,7 +293,7 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
 // F = NoFuse: tails are written to a.tails.  F = WCfg<...>: each batch of
 // tails is written in place into the staged rows (group starts become zero
 // rows) and absorbed into the warp's TSQR accumulator Racc.
-template <int SLOTS, int VEC, class F, class SM, class RA>
+template <int SLOTS, int VEC, class F, bool VJ, class SM, class RA>
 __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
                              int64_t u, int lane, RA& Racc) {
   constexpr bool FUSED = !std::is_same<F, NoFuse>::value;
@@ -183,6 +303,13 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
   const int64_t p1 = min(p0 + kUnit, a.n_rows);
   int64_t g = a.ufirst ? (int64_t)a.ufirst[u] : seg_of(a.begins, p0, 0, a.n_seg);
   const int grp = lane / geo.L, cl = lane % geo.L;
+  // Join-on-read: the block (child or own) of each owned column packet.
+  int cs[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    int rel = 0;
+    cs[s] = VJ ? vj_span(a, VEC * (cl + geo.L * s), rel) : 0;
+  }
 
   // Running prefix (per owned column) carried into the next batch.
   double S[SLOTS][VEC];
@@ -226,7 +353,8 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
 
   for (int64_t pb = p0; pb < p1; pb += a.rb) {
     const int nb = (int)(p1 - pb < (int64_t)a.rb ? p1 - pb : (int64_t)a.rb);
-    if (w > 0) stage_rows<SLOTS, VEC>(a, geo, sm, pb, nb, lane);
+    if (w > 0) stage_rows<SLOTS, VEC, VJ>(a, geo, sm, pb, nb, lane);
+    else if (VJ) __syncwarp();
     // Group starts inside the batch (groups g+1 .. g+nb can start here):
     // flagged in shared memory, then each row's group is g plus a ballot
     // prefix count -- one level of loads instead of a binary search per row.
@@ -258,7 +386,8 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         jj = p - b0;
         m = b1 - b0;
         fl = (jj == 0 ? 1 : 0) | (p == b1 - 1 ? 2 : 0);
-        if (weighted) v = a.weights[src_row(a, p)];
+        if (VJ) v = sm.wt[rr];
+        else if (weighted) v = a.weights[src_row(a, p)];
       }
       double ts = 1.0;
       if (live && a.tail_count) ts = sqrt((double)a.tail_count[sg]);  // exact for squares
@@ -348,6 +477,11 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
           } else {
             x[0] = row[pk];
           }
+          if (VJ) {
+            const double fc = sm.vjf[rr][cs[s]];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) x[e] *= fc;
+          }
 #pragma unroll
           for (int e = 0; e < VEC; ++e) {
             const double base_ = (fl & 1) ? 0.0 : loc[s][e];
@@ -411,6 +545,11 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
           } else {
             x[0] = row[pk];
           }
+          if (VJ) {
+            const double fc = sm.vjf[rr][cs[s]];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) x[e] *= fc;
+          }
 #pragma unroll
           for (int e = 0; e < VEC; ++e) {
             if (sf.y & 1) run[s][e] = 0.0;
@@ -462,21 +601,22 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
   }
 }
 
-template <int SLOTS, int VEC>
+template <int SLOTS, int VEC, bool VJ>
 __global__ void __launch_bounds__(kWarps * 32)
     k_heads_tails(HtDev a, Geo geo) {
+  using SMT = std::conditional_t<VJ, WarpSmemVJ, WarpSmem>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpSmem* all = reinterpret_cast<WarpSmem*>(smem_raw);
+  SMT* all = reinterpret_cast<SMT*>(smem_raw);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  WarpSmem& sm = all[warp];
+  SMT& sm = all[warp];
   int dummy = 0;
   while (true) {
     int64_t u = 0;
     if (lane == 0) u = atomicAdd(a.ticket, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= a.n_units) break;
-    process_unit<SLOTS, VEC, NoFuse>(a, geo, sm, u, lane, dummy);
+    process_unit<SLOTS, VEC, NoFuse, VJ>(a, geo, sm, u, lane, dummy);
   }
 }
 
@@ -497,13 +637,11 @@ __global__ void __launch_bounds__(kWarps * 32, F::MINB)
   for (int m = 0; m < F::RR; ++m)
 #pragma unroll
     for (int q = 0; q < F::CPT; ++q) Racc[m][q] = 0.0;
-  while (true) {
-    int64_t u = 0;
-    if (lane == 0) u = atomicAdd(a.ticket, 1);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= a.n_units) break;
-    process_unit<1, VEC, F>(a, geo, sm, u, lane, Racc);
-  }
+  // Static unit -> warp assignment: which rows each accumulator absorbs
+  // (and so the rounding of R) depends only on the grid, not on timing.
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t u = (int64_t)blockIdx.x * kWarps + warp; u < a.n_units; u += nw)
+    process_unit<1, VEC, F, false>(a, geo, sm, u, lane, Racc);
   const int r = lane % F::TR, c = lane / F::TR;
   double* o = partials + ((int64_t)blockIdx.x * kWarps + warp) * F::W * F::W;
 #pragma unroll
@@ -562,6 +700,20 @@ __global__ void k_unit_tail_sums(HtDev a, int* __restrict__ cont,
 #pragma unroll 4
       for (int64_t p = q0 + grp; p < p1; p += geo.G) {
         const int64_t r = src_row(a, p);
+        if (a.nj >= 0) {
+          double x[VEC], v = 1.0;
+          if (pk < np) {
+            vj_load<VEC>(a, r, VEC * pk, x, v);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) s[e] = fma(v, x[e], s[e]);
+          } else {
+            double f[kVJMax + 1];
+            int idx[kVJMax];
+            v = vj_row(a, r, f, idx);
+          }
+          nacc = fma(v, v, nacc);
+          continue;
+        }
         const double v = weighted ? a.weights[r] : 1.0;
         if (pk < np) {
           const double* src = a.data + r * a.ld + VEC * pk;
@@ -793,10 +945,10 @@ __global__ void __launch_bounds__(256) k_join_elems2(const __grid_constant__ Joi
   }
 }
 
-template <int SLOTS, int VEC>
+template <int SLOTS, int VEC, bool VJ>
 void launch_main(Context& ctx, const HtDev& d, const Geo& geo) {
-  const size_t smem = sizeof(WarpSmem) * kWarps;
-  auto kern = k_heads_tails<SLOTS, VEC>;
+  const size_t smem = (VJ ? sizeof(WarpSmemVJ) : sizeof(WarpSmem)) * kWarps;
+  auto kern = k_heads_tails<SLOTS, VEC, VJ>;
   FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   int per_sm = 0;
@@ -815,11 +967,17 @@ void launch_main(Context& ctx, const HtDev& d, const Geo& geo) {
 template <int VEC>
 void launch_slots(Context& ctx, const HtDev& d, const Geo& geo) {
   const int slots = (geo.np + geo.L - 1) / geo.L;
-  if (slots <= 1) launch_main<1, VEC>(ctx, d, geo);
-  else if (slots <= 2) launch_main<2, VEC>(ctx, d, geo);
-  else if (slots <= 4) launch_main<4, VEC>(ctx, d, geo);
-  else if (slots <= 8) launch_main<8, VEC>(ctx, d, geo);
-  else launch_main<16, VEC>(ctx, d, geo);
+  if (d.nj >= 0) {  // join-on-read: widths up to 4 packets per lane
+    if (slots <= 1) launch_main<1, VEC, true>(ctx, d, geo);
+    else if (slots <= 2) launch_main<2, VEC, true>(ctx, d, geo);
+    else launch_main<4, VEC, true>(ctx, d, geo);
+    return;
+  }
+  if (slots <= 1) launch_main<1, VEC, false>(ctx, d, geo);
+  else if (slots <= 2) launch_main<2, VEC, false>(ctx, d, geo);
+  else if (slots <= 4) launch_main<4, VEC, false>(ctx, d, geo);
+  else if (slots <= 8) launch_main<8, VEC, false>(ctx, d, geo);
+  else launch_main<16, VEC, false>(ctx, d, geo);
 }
 
 }  // namespace
@@ -832,6 +990,18 @@ struct HtPrep {
   DevArray<int> cont, ticket, ufirst;
   DevArray<double> val, carry;
 };
+
+// double2 staging of joined rows: every block starts on an even column and
+// every source row on a 16-byte boundary.
+static bool vj_vec2_ok(const HeadTailArgs& in) {
+  const JoinArgs& j = *in.join;
+  bool ok = j.own_w % 2 == 0 && in.join_ldh % 2 == 0 &&
+            reinterpret_cast<uintptr_t>(in.join_heads) % 16 == 0;
+  for (int c = 0; c < j.n_children; ++c)
+    ok = ok && j.child_off[c] % 2 == 0 && j.child_w[c] % 2 == 0 &&
+         reinterpret_cast<uintptr_t>(j.child_S[c]) % 16 == 0;
+  return ok;
+}
 
 static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixed) {
   HtDev& d = P.d;
@@ -852,7 +1022,25 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   d.tails = in.tails;
   d.ldt = in.ldt;
   d.scales = in.scales;
-  d.rb = in.w > 0 ? std::max(1, std::min(kMaxRB, kSmemDoubles / in.w)) : kMaxRB;
+  d.nj = -1;
+  if (in.join) {
+    const JoinArgs& j = *in.join;
+    if (j.n_children > kVJMax) fail(FG_E_ARG, "join-on-read: too many children");
+    d.nj = j.n_children;
+    d.own_w = j.own_w;
+    d.jhead = in.join_heads;
+    d.jld = in.join_ldh;
+    for (int c = 0; c < j.n_children; ++c) {
+      d.jlidx[c] = j.lidx[c];
+      d.jS[c] = j.child_S[c];
+      d.jscale[c] = j.child_scale[c];
+      d.jw[c] = j.child_w[c];
+      d.joff[c] = j.child_off[c];
+    }
+  }
+  d.rb = in.w > 0 ? std::max(1, std::min(in.join ? kVJRows : kMaxRB, kSmemDoubles / in.w))
+                  : kMaxRB;
+  if (in.join && in.w == 0) fail(FG_E_ARG, "join-on-read needs data columns");
   d.n_units = ceil_div(in.n_rows, kUnit);
 
   const int V = in.w + (in.weights ? 1 : 0);
@@ -876,8 +1064,9 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
                   threads, 0, ctx.stream>>>(d, cont.get(), P.ufirst.get(), any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
-    const bool vec2 = in.w % 2 == 0 && in.ld % 2 == 0 &&
-                      reinterpret_cast<uintptr_t>(in.data) % 16 == 0;
+    const bool vec2 = in.join ? vj_vec2_ok(in)
+                              : in.w % 2 == 0 && in.ld % 2 == 0 &&
+                                    reinterpret_cast<uintptr_t>(in.data) % 16 == 0;
     Geo tg{};
     tg.vec = vec2 ? 2 : 1;
     tg.np = in.w > 0 ? (in.w + tg.vec - 1) / tg.vec : 1;
@@ -915,8 +1104,10 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   }
   // Vector width, lanes per row-group and rows per batch.
   Geo& geo = P.geo;
-  const bool aligned = in.w > 0 && in.w % 2 == 0 && in.ld % 2 == 0 &&
-                       (reinterpret_cast<uintptr_t>(in.data) % 16 == 0) &&
+  const bool src_ok = in.join ? vj_vec2_ok(in)
+                              : in.ld % 2 == 0 &&
+                                    reinterpret_cast<uintptr_t>(in.data) % 16 == 0;
+  const bool aligned = in.w > 0 && in.w % 2 == 0 && src_ok &&
                        (!in.tails || (in.ldt % 2 == 0 &&
                                       reinterpret_cast<uintptr_t>(in.tails) % 16 == 0));
   geo.vec = aligned ? 2 : 1;
@@ -925,7 +1116,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   while (geo.L < geo.np && geo.L < 32) geo.L <<= 1;
   geo.G = 32 / geo.L;
   if (in.w > 0) {
-    int rb = std::min(kMaxRB, kSmemDoubles / in.w);
+    int rb = std::min(in.join ? kVJRows : kMaxRB, kSmemDoubles / in.w);
     if (rb >= geo.G) rb -= rb % geo.G;
     d.rb = std::max(1, rb);
   }

@@ -117,6 +117,7 @@ void launch_up_div(Context& ctx, uint64_t* phi_up, const uint64_t* phi_down,
                    int64_t P, unsigned* status);
 
 // ---- headtail.cu ----------------------------------------------------------
+struct JoinArgs;
 struct HeadTailArgs {
   const double* data = nullptr;
   int64_t ld = 0;
@@ -134,6 +135,13 @@ struct HeadTailArgs {
   double* tails = nullptr;
   int64_t ldt = 0;
   double* scales = nullptr;
+  // Join-on-read (project-away of a joined node, K4 folded into K5): rows
+  // are the join of own heads (join_heads, row stride join_ldh) and the
+  // children's summaries described by *join (S and scale of *join unused);
+  // `data`/`ld` are ignored and `weights` are the own (pre-join) scales.
+  const JoinArgs* join = nullptr;
+  const double* join_heads = nullptr;
+  int64_t join_ldh = 0;
 };
 // Runs the segmented (generalized) head/tail transform.  Needs the max
 // segment size only to decide whether the heavy-segment pre-pass runs.

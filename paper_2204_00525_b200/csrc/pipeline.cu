@@ -616,10 +616,17 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     const bool is_leaf = n.children.empty();
     const int64_t G = n.grp.G;
     n.width = lay.sub_end[i] - lay.sub_begin[i];
+    // Join-on-read: an inner node's joined summary rows are consumed only
+    // by its project-away, which builds them on the fly from the own heads
+    // and the children's summaries -- S holds just the heads (C3's fact
+    // node: 54 M x 8 instead of 54 M x 20 written, read and re-read).
+    const bool vj = !is_root && !is_leaf && n.width > 0 &&
+                    (int)n.children.size() <= 4 && getenv("FG_NO_JOIN_ON_READ") == nullptr;
+    const int64_t ldS = vj ? n.w : n.width;
     // Every element of S is written: own columns by the heads (one per
     // group), child columns by the join (zero for a missing child), so no
     // memset (8.6 GB on C3's fact node).
-    n.S.alloc(G * n.width, st);
+    n.S.alloc(G * std::max<int64_t>(ldS, 1), st);
     n.scale.alloc(G, st);
     const int64_t n_tails = n.rows - G;
     // The fused kernel absorbs a zero row per group start; when groups are
@@ -640,7 +647,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     a.tail_count = n.circ.get();
     a.head_index = (is_leaf && !is_root) ? n.pidx.get() : nullptr;
     a.heads = n.w > 0 ? n.S.get() : nullptr;
-    a.ldh = n.width;
+    a.ldh = ldS;
     a.tails = n.tails.get();
     a.ldt = n.w;
     a.scales = n.scale.get();
@@ -664,8 +671,8 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       ++fused_launches;
       fused_flops += span_flops((double)n_tails, n.w);
     }
+    JoinArgs j{};
     if (!is_leaf) {
-      JoinArgs j{};
       j.G = G;
       j.own_w = n.w;
       j.S = n.S.get();
@@ -682,8 +689,10 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
         j.child_w[k] = (int)c.width;
         j.child_off[k] = (int)(lay.sub_begin[n.children[k]] - lay.sub_begin[i]);
       }
-      launch_join(ctx, j);
-      std::swap(n.scale, n.scale_j);  // joined scales replace the head scales
+      if (!vj) {
+        launch_join(ctx, j);
+        std::swap(n.scale, n.scale_j);  // joined scales replace the head scales
+      }
     }
     if (!is_root && !is_leaf) {
       n.Sq.alloc(n.P * n.width, st);
@@ -696,6 +705,12 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       b.data = n.S.get();
       b.ld = n.width;
       b.w = (int)n.width;
+      if (vj) {
+        b.data = nullptr;
+        b.join = &j;
+        b.join_heads = n.S.get();
+        b.join_ldh = ldS;
+      }
       b.perm = n.pa_perm.get();
       b.begins = n.pa_begins.get();
       b.n_seg = n.P;
@@ -719,10 +734,14 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
         kt_ht.begin();
         run_heads_tails(ctx, b);
         kt_ht.end();
-        // summary rows read once, parent-key heads and projection tails
-        // written once
-        ht_bytes += 8.0 * ((double)G * n.width + (double)n.P * n.width +
-                           (double)(G - n.P) * n.width);
+        // summary rows read once (join-on-read: the own heads; the
+        // children's summaries are L2-resident lookups), parent-key heads
+        // and projection tails written once
+        double child_rows = 0;
+        if (vj)
+          for (int c : n.children) child_rows += (double)nodes[c]->P * nodes[c]->width;
+        ht_bytes += 8.0 * ((double)G * (vj ? n.w : n.width) + child_rows +
+                           (double)n.P * n.width + (double)(G - n.P) * n.width);
       }
       n.sum_S = n.Sq.get();
       n.sum_scale = n.scale_q.get();

@@ -200,12 +200,19 @@ def test_errors_match_reference_taxonomy():
         run_gpu(db)
 
 
-def test_determinism_and_launch_evidence():
-    db = workloads.make("C5", seed=5, scale=0.003)
+@pytest.mark.parametrize("cfg,scale", [("C5", 0.003), ("C2", 0.05), ("C3", 0.002),
+                                       ("C4", 0.02)])
+def test_determinism_and_launch_evidence(cfg, scale):
+    """R bit-identical run to run -- including C2, whose own tails take the
+    fused heads/tails -> TSQR kernel (static unit -> warp assignment)."""
+    db = workloads.make(cfg, seed=5, scale=scale)
     r1, R1 = run_gpu(db)
-    r2, R2 = run_gpu(db)
-    assert np.array_equal(R1, R2), "R must be bit-identical run to run"
+    Rs = [run_gpu(db)[1] for _ in range(3)]
+    for R2 in Rs:
+        assert np.array_equal(R1, R2), "R must be bit-identical run to run"
     assert r1.kernels > 10
+    if cfg == "C2":
+        assert r1.fused_launches == 2
 
 
 def test_full_size_c2_gram_property():
