@@ -176,7 +176,8 @@ FG_API fg_status fg_get_r0_span(fg_ctx* ctx, int32_t idx, int32_t* node,
 
 /* ---- phase-level kernels (device pointers, context stream) ------------- */
 
-/* K1: stable grouping of packed keys.  keys[n] uses the low `bits` bits.
+/* K1: stable grouping of packed keys; every keys[i] < 2^bits (bits <= 32 runs
+ * the 32-bit key path the pipeline uses for narrow keys).
  * Writes perm[n] (stable sort permutation), begins[G+1] and uniq[G]
  * (capacity n+1 / n), and *G (host).  relation.hpp:56-66,127-167 */
 FG_API fg_status fg_group_keys(fg_ctx* ctx, const uint64_t* keys, int64_t n,

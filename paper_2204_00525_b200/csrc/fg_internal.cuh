@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <utility>
@@ -55,6 +56,12 @@ struct Context;
 class BlockCache {
  public:
   void* get(size_t bytes) {
+    if (exact()) {  // sanitizer runs: every buffer its own exact allocation
+      void* p = nullptr;
+      FG_CUDA(cudaMalloc(&p, bytes ? bytes : 1));
+      live_[p] = bytes;
+      return p;
+    }
     bytes = round(bytes);
     auto it = free_.lower_bound(bytes);
     if (it != free_.end() && it->first <= bytes + bytes / 4 + (1 << 20)) {
@@ -78,6 +85,11 @@ class BlockCache {
   void put(void* p) {
     auto it = live_.find(p);
     if (it == live_.end()) return;
+    if (exact()) {  // cudaFree waits for the device, so in-flight users finish first
+      live_.erase(it);
+      cudaFree(p);
+      return;
+    }
     free_.emplace(it->second, p);
     live_.erase(it);
   }
@@ -92,6 +104,12 @@ class BlockCache {
     free_.clear();
   }
   size_t reserved() const { return reserved_; }
+  // FG_EXACT_ALLOC=1: no caching or rounding, so compute-sanitizer memcheck
+  // sees every out-of-bounds access.
+  static bool exact() {
+    static const bool e = getenv("FG_EXACT_ALLOC") != nullptr;
+    return e;
+  }
 
  private:
   static size_t round(size_t b) {

@@ -6,15 +6,10 @@
 //   * an order-preserving packing of each int64 key tuple into one u64
 //     (per-attribute offset encoding, fields in declaration order, most
 //     significant first) -- lexicographic tuple order == integer order;
-//   * a stable LSD radix sort over only the significant bits (CUB onesweep
-//     templates instantiated for sm_100a) carrying the row permutation;
-//   * run-length extraction of the segment offsets;
+//   * a stable LSD radix sort over only the significant bits carrying the
+//     row permutation, and segment-offset extraction (radix.cu);
 //   * field re-packing for projections onto parent-shared attributes, and
 //     binary search of projected keys in the child's sorted key table.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_run_length_encode.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include "launchers.cuh"
 
 namespace fg {
@@ -31,27 +26,41 @@ inline int grid_for(const Context& ctx, int64_t n, int per_sm = 8) {
   return static_cast<int>(g);
 }
 
+// Min/max of every key column in one pass over the row-major key tuples
+// (grid-stride over rows; per-column warp reduction, then atomics).
 __global__ void k_key_minmax(const int64_t* __restrict__ keys, int64_t rows,
                              int n_key, const int* __restrict__ attr_of_col,
                              long long* mins, long long* maxs) {
-  // One column at a time through blockIdx.y; grid-stride over rows.
-  const int c = blockIdx.y;
-  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  long long lo[kMaxKeyCols], hi[kMaxKeyCols];
+#pragma unroll
+  for (int c = 0; c < kMaxKeyCols; ++c) {
+    lo[c] = LLONG_MAX;
+    hi[c] = LLONG_MIN;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
        i += (int64_t)gridDim.x * blockDim.x) {
-    long long v = keys[i * n_key + c];
-    lo = v < lo ? v : lo;
-    hi = v > hi ? v : hi;
+#pragma unroll
+    for (int c = 0; c < kMaxKeyCols; ++c) {
+      if (c >= n_key) break;
+      const long long v = keys[i * n_key + c];
+      lo[c] = v < lo[c] ? v : lo[c];
+      hi[c] = v > hi[c] ? v : hi[c];
+    }
   }
-  for (int o = 16; o; o >>= 1) {
-    long long a = __shfl_xor_sync(0xffffffffu, lo, o);
-    long long b = __shfl_xor_sync(0xffffffffu, hi, o);
-    lo = a < lo ? a : lo;
-    hi = b > hi ? b : hi;
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin(&mins[attr_of_col[c]], lo);
-    atomicMax(&maxs[attr_of_col[c]], hi);
+#pragma unroll
+  for (int c = 0; c < kMaxKeyCols; ++c) {
+    if (c >= n_key) break;
+    long long a = lo[c], b = hi[c];
+    for (int o = 16; o; o >>= 1) {
+      const long long x = __shfl_xor_sync(0xffffffffu, a, o);
+      const long long y = __shfl_xor_sync(0xffffffffu, b, o);
+      a = x < a ? x : a;
+      b = y > b ? y : b;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&mins[attr_of_col[c]], a);
+      atomicMax(&maxs[attr_of_col[c]], b);
+    }
   }
 }
 
@@ -146,25 +155,17 @@ __global__ void k_unpack(const uint64_t* __restrict__ in, int64_t n,
   }
 }
 
+__global__ void k_narrow(const uint64_t* __restrict__ in, int64_t n,
+                         uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = static_cast<uint32_t>(in[i]);
+}
+
 __global__ void k_iota(int* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = static_cast<int>(i);
-}
-
-__global__ void k_head_flags(const uint64_t* __restrict__ sorted, int64_t n,
-                             int* __restrict__ flags) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    flags[i] = (i == 0 || sorted[i] != sorted[i - 1]) ? 1 : 0;
-}
-
-__global__ void k_scatter_runs(const int* __restrict__ scan,
-                               const int* __restrict__ perm, int64_t n,
-                               int* __restrict__ pidx) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    pidx[perm[i]] = scan[i] - 1;
 }
 
 __global__ void k_seg_sizes(const int* __restrict__ begins, int64_t G,
@@ -174,24 +175,15 @@ __global__ void k_seg_sizes(const int* __restrict__ begins, int64_t G,
     sizes[i] = (uint64_t)(begins[i + 1] - begins[i]);
 }
 
-__global__ void k_set_last(int* begins, int64_t G, int n) { begins[G] = n; }
-
-__global__ void k_widen(const uint32_t* __restrict__ in, int64_t n,
-                        uint64_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = in[i];
-}
-
 }  // namespace
 
 void launch_key_minmax(Context& ctx, const int64_t* keys, int64_t rows,
                        int n_key, const int* attr_of_col_dev, long long* mins,
                        long long* maxs) {
   if (rows == 0 || n_key == 0) return;
-  dim3 grid(grid_for(ctx, rows, 4), n_key);
-  k_key_minmax<<<grid, kThreads, 0, ctx.stream>>>(keys, rows, n_key,
-                                                  attr_of_col_dev, mins, maxs);
+  if (n_key > kMaxKeyCols) fail(FG_E_UNSUPPORTED, "more than 16 key columns");
+  k_key_minmax<<<grid_for(ctx, rows, 4), kThreads, 0, ctx.stream>>>(keys, rows, n_key,
+                                                                   attr_of_col_dev, mins, maxs);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
 }
@@ -251,6 +243,13 @@ void launch_unpack(Context& ctx, const uint64_t* in, int64_t n,
   FG_KERNEL_CHECK();
 }
 
+void launch_narrow(Context& ctx, const uint64_t* in, int64_t n, uint32_t* out) {
+  if (n == 0) return;
+  k_narrow<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(in, n, out);
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
+}
+
 void launch_iota(Context& ctx, int* out, int64_t n) {
   if (n == 0) return;
   k_iota<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(out, n);
@@ -266,164 +265,78 @@ void launch_seg_sizes(Context& ctx, const int* begins, int64_t G,
   FG_KERNEL_CHECK();
 }
 
-template <class KeyT>
-void sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out,
-                const int* vals_in, int* vals_out, int64_t n, int bits) {
-  if (n == 0) return;
-  if (bits == 0) {
-    FG_CUDA(cudaMemcpyAsync(keys_out, keys_in, n * sizeof(KeyT),
-                            cudaMemcpyDeviceToDevice, ctx.stream));
-    FG_CUDA(cudaMemcpyAsync(vals_out, vals_in, n * sizeof(int),
-                            cudaMemcpyDeviceToDevice, ctx.stream));
-    return;
-  }
-  size_t temp = 0;
-  FG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys_in, keys_out,
-                                          vals_in, vals_out, n, 0, bits,
-                                          ctx.stream));
-  DevArray<unsigned char> tmp(temp, ctx.stream);
-  FG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), temp, keys_in, keys_out,
-                                          vals_in, vals_out, n, 0, bits,
-                                          ctx.stream));
-  ctx.launches += (bits + 7) / 8 + 1;
-}
-
-template <class KeyT>
-void run_length(Context& ctx, const KeyT* sorted, int64_t n,
-                KeyT* uniq, int* counts, int64_t* num_runs_dev) {
-  size_t temp = 0;
-  FG_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, temp, sorted, uniq,
-                                             counts, num_runs_dev, n,
-                                             ctx.stream));
-  DevArray<unsigned char> tmp(temp, ctx.stream);
-  FG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), temp, sorted, uniq,
-                                             counts, num_runs_dev, n,
-                                             ctx.stream));
-  ctx.launches += 2;
-}
-
 void exclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n) {
-  if (n == 0) return;
-  size_t temp = 0;
-  FG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, in, out, n, ctx.stream));
-  DevArray<unsigned char> tmp(temp, ctx.stream);
-  FG_CUDA(
-      cub::DeviceScan::ExclusiveSum(tmp.get(), temp, in, out, n, ctx.stream));
-  ctx.launches += 2;
+  scan_int(ctx, in, out, n, false);
 }
 
 void inclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n) {
-  if (n == 0) return;
-  size_t temp = 0;
-  FG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, in, out, n, ctx.stream));
-  DevArray<unsigned char> tmp(temp, ctx.stream);
-  FG_CUDA(
-      cub::DeviceScan::InclusiveSum(tmp.get(), temp, in, out, n, ctx.stream));
-  ctx.launches += 2;
+  scan_int(ctx, in, out, n, true);
 }
 
-void launch_run_ids(Context& ctx, const uint64_t* sorted, const int* perm,
-                    int64_t n, int* flags, int* scan, int* pidx) {
-  if (n == 0) return;
-  k_head_flags<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(sorted, n, flags);
-  FG_LAUNCHED(ctx);
-  FG_KERNEL_CHECK();
-  inclusive_sum_int(ctx, flags, scan, n);
-  k_scatter_runs<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(scan, perm, n,
-                                                                pidx);
-  FG_LAUNCHED(ctx);
-  FG_KERNEL_CHECK();
-}
-
-// Two-phase grouping so several relations can be sorted before one host
-// synchronisation reads all the group counts.
+// Grouping is split so several relations can be sorted before one host
+// synchronisation reads all the group counts: begin = radix sort (radix.cu)
+// + segment extraction into upper-bound (n-row) buffers; finish = adopt them
+// once G is known.
 template <class KeyT>
 void group_begin_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
-                   const int* perm_in, GroupOut& out, GroupPending& pend) {
-  out.perm.alloc(n, ctx.stream);
+                   const int* perm_in, GroupOut& out, GroupPending& pend,
+                   const uint32_t* hist, int* pidx) {
+  cudaStream_t st = ctx.stream;
+  out.perm.alloc(n, st);
   pend.n = n;
-  pend.wide = sizeof(KeyT) == 8;
-  DevArray<KeyT>& sorted = *reinterpret_cast<DevArray<KeyT>*>(
-      pend.wide ? (void*)&pend.sorted64 : (void*)&pend.sorted32);
-  DevArray<KeyT>& uniq = *reinterpret_cast<DevArray<KeyT>*>(
-      pend.wide ? (void*)&pend.uniq64 : (void*)&pend.uniq32);
-  sorted.alloc(n, ctx.stream);
-  sort_pairs<KeyT>(ctx, keys, sorted.get(), perm_in, out.perm.get(), n, bits);
-  uniq.alloc(n, ctx.stream);
-  pend.counts.alloc(n + 1, ctx.stream);
-  pend.nr.alloc(1, ctx.stream);
-  if (n) run_length<KeyT>(ctx, sorted.get(), n, uniq.get(), pend.counts.get(), pend.nr.get());
-  else pend.nr.zero();
+  pend.begins.alloc(n + 1, st);
+  pend.uniq.alloc(n, st);
+  pend.nr.alloc(1, st);
+  DevArray<KeyT> sorted(n, st);
+  radix_sort_pairs<KeyT>(ctx, keys, sorted.get(), perm_in, out.perm.get(), n, bits, hist);
+  launch_segments<KeyT>(ctx, sorted.get(), n, pend.begins.get(), pend.uniq.get(),
+                        pend.nr.get(), out.perm.get(), pidx);
 }
 
 void group_finish(Context& ctx, int64_t G, GroupOut& out, GroupPending& pend) {
-  const int64_t n = pend.n;
+  (void)ctx;
   out.G = G;
-  out.begins.alloc(G + 1, ctx.stream);
-  exclusive_sum_int(ctx, pend.counts.get(), out.begins.get(), G);
-  k_set_last<<<1, 1, 0, ctx.stream>>>(out.begins.get(), G, static_cast<int>(n));
-  FG_LAUNCHED(ctx);
-  out.uniq.alloc(G, ctx.stream);
-  if (G) {
-    if (pend.wide) {
-      FG_CUDA(cudaMemcpyAsync(out.uniq.get(), pend.uniq64.get(), G * sizeof(uint64_t),
-                              cudaMemcpyDeviceToDevice, ctx.stream));
-    } else {
-      k_widen<<<grid_for(ctx, G), kThreads, 0, ctx.stream>>>(pend.uniq32.get(), G,
-                                                            out.uniq.get());
-      FG_LAUNCHED(ctx);
-      FG_KERNEL_CHECK();
-    }
-  }
-  if (pend.keep_sorted) {
-    if (pend.wide) {
-      out.sorted = std::move(pend.sorted64);
-    } else {
-      out.sorted.alloc(n, ctx.stream);
-      k_widen<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(pend.sorted32.get(), n,
-                                                            out.sorted.get());
-      FG_LAUNCHED(ctx);
-      FG_KERNEL_CHECK();
-    }
-  }
+  out.begins = std::move(pend.begins);
+  out.uniq = std::move(pend.uniq);
   pend = GroupPending();
 }
 
 void group_begin(Context& ctx, const uint64_t* keys, int64_t n, int bits,
-                 const int* perm_in, GroupOut& out, GroupPending& pend) {
-  group_begin_t<uint64_t>(ctx, keys, n, bits, perm_in, out, pend);
+                 const int* perm_in, GroupOut& out, GroupPending& pend,
+                 const uint32_t* hist, int* pidx) {
+  group_begin_t<uint64_t>(ctx, keys, n, bits, perm_in, out, pend, hist, pidx);
 }
 void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
-                   const int* perm_in, GroupOut& out, GroupPending& pend) {
-  group_begin_t<uint32_t>(ctx, keys, n, bits, perm_in, out, pend);
+                   const int* perm_in, GroupOut& out, GroupPending& pend,
+                   const uint32_t* hist, int* pidx) {
+  group_begin_t<uint32_t>(ctx, keys, n, bits, perm_in, out, pend, hist, pidx);
 }
 
 void group_begin_presorted(Context& ctx, const uint64_t* keys, int64_t n,
-                           const int* perm_in, GroupOut& out, GroupPending& pend) {
-  out.perm.alloc(n, ctx.stream);
+                           const int* perm_in, GroupOut& out, GroupPending& pend,
+                           int* pidx) {
+  cudaStream_t st = ctx.stream;
+  out.perm.alloc(n, st);
   pend.n = n;
-  pend.wide = true;
-  pend.sorted64.alloc(n, ctx.stream);
+  pend.begins.alloc(n + 1, st);
+  pend.uniq.alloc(n, st);
+  pend.nr.alloc(1, st);
   if (n) {
-    FG_CUDA(cudaMemcpyAsync(out.perm.get(), perm_in, n * sizeof(int),
-                            cudaMemcpyDeviceToDevice, ctx.stream));
-    FG_CUDA(cudaMemcpyAsync(pend.sorted64.get(), keys, n * sizeof(uint64_t),
-                            cudaMemcpyDeviceToDevice, ctx.stream));
+    if (perm_in)
+      FG_CUDA(cudaMemcpyAsync(out.perm.get(), perm_in, n * sizeof(int),
+                              cudaMemcpyDeviceToDevice, st));
+    else
+      launch_iota(ctx, out.perm.get(), n);
   }
-  pend.uniq64.alloc(n, ctx.stream);
-  pend.counts.alloc(n + 1, ctx.stream);
-  pend.nr.alloc(1, ctx.stream);
-  if (n) run_length<uint64_t>(ctx, pend.sorted64.get(), n, pend.uniq64.get(),
-                              pend.counts.get(), pend.nr.get());
-  else pend.nr.zero();
+  launch_segments<uint64_t>(ctx, keys, n, pend.begins.get(), pend.uniq.get(), pend.nr.get(),
+                            perm_in, pidx);
 }
 
 template <class KeyT>
 void group_sorted_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
-                    const int* perm_in, GroupOut& out, bool keep_sorted) {
+                    const int* perm_in, GroupOut& out) {
   GroupPending pend;
-  pend.keep_sorted = keep_sorted;
-  group_begin_t<KeyT>(ctx, keys, n, bits, perm_in, out, pend);
+  group_begin_t<KeyT>(ctx, keys, n, bits, perm_in, out, pend, nullptr, nullptr);
   int64_t G = 0;
   FG_CUDA(cudaMemcpyAsync(&G, pend.nr.get(), sizeof G, cudaMemcpyDeviceToHost,
                           ctx.stream));
@@ -432,13 +345,13 @@ void group_sorted_t(Context& ctx, const KeyT* keys, int64_t n, int bits,
 }
 
 void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
-                  const int* perm_in, GroupOut& out, bool keep_sorted) {
-  group_sorted_t<uint64_t>(ctx, keys, n, bits, perm_in, out, keep_sorted);
+                  const int* perm_in, GroupOut& out) {
+  group_sorted_t<uint64_t>(ctx, keys, n, bits, perm_in, out);
 }
 
 void group_sorted32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
-                    const int* perm_in, GroupOut& out, bool keep_sorted) {
-  group_sorted_t<uint32_t>(ctx, keys, n, bits, perm_in, out, keep_sorted);
+                    const int* perm_in, GroupOut& out) {
+  group_sorted_t<uint32_t>(ctx, keys, n, bits, perm_in, out);
 }
 
 template void launch_pack_keys<uint64_t>(Context&, const int64_t*, int64_t, int,

@@ -58,9 +58,10 @@ void build_tree(std::vector<std::unique_ptr<Node>>& nodes, int root,
     fail(FG_E_TREE, "join tree: not a connected tree");
 }
 
-// join_tree.hpp:104-180 (path property, every key attribute shared, data
-// attribute names disjoint from everything else) + canonicalize's schema
-// checks (relation.hpp:128-146).
+// The checks of join_tree.hpp:104-180 (path property, every key attribute
+// shared, data attribute names disjoint from everything else), restated as
+// a connectivity count with a depth-based path walk for the error report,
+// plus canonicalize's schema checks (relation.hpp:128-146).
 template <class Node>
 void validate(const std::vector<std::unique_ptr<Node>>& nodes) {
   for (const auto& n : nodes) {
@@ -77,50 +78,67 @@ void validate(const std::vector<std::unique_ptr<Node>>& nodes) {
   }
   const int r = (int)nodes.size();
   if (r <= 1) return;
-  auto path_between = [&](int a, int b) {
-    std::vector<int> up_a, up_b;
-    for (int x = a; x != -1; x = nodes[x]->parent) up_a.push_back(x);
-    for (int x = b; x != -1; x = nodes[x]->parent) up_b.push_back(x);
-    std::set<int> anc(up_a.begin(), up_a.end());
-    int meet = -1;
-    for (int x : up_b)
-      if (anc.count(x)) { meet = x; break; }
-    std::vector<int> path;
-    for (int x : up_a) { path.push_back(x); if (x == meet) break; }
-    std::vector<int> down;
-    for (int x : up_b) { if (x == meet) break; down.push_back(x); }
-    path.insert(path.end(), down.rbegin(), down.rend());
-    return path;
+  // Depth of every node; the tree path a -> b is a's ancestor chain up to
+  // their lowest common ancestor followed by b's chain back down.
+  std::vector<int> depth(r, 0);
+  for (int i = 0; i < r; ++i)
+    for (int x = nodes[i]->parent; x != -1; x = nodes[x]->parent) ++depth[i];
+  std::vector<std::set<std::string>> has(r);
+  for (int i = 0; i < r; ++i) has[i].insert(nodes[i]->key_names.begin(), nodes[i]->key_names.end());
+  // First node on the path a -> b (in path order) lacking `attr`, or -1.
+  auto first_gap = [&](int a, int b, const std::string& attr) {
+    std::vector<int> down;  // b's side, collected bottom-up
+    int x = a, y = b;
+    std::vector<int> up;
+    while (depth[x] > depth[y]) { up.push_back(x); x = nodes[x]->parent; }
+    while (depth[y] > depth[x]) { down.push_back(y); y = nodes[y]->parent; }
+    while (x != y) {
+      up.push_back(x);
+      down.push_back(y);
+      x = nodes[x]->parent;
+      y = nodes[y]->parent;
+    }
+    up.push_back(x);  // the common ancestor
+    up.insert(up.end(), down.rbegin(), down.rend());
+    for (int n : up)
+      if (!has[n].count(attr)) return n;
+    return -1;
   };
-  std::map<std::string, std::vector<int>> attr_nodes;
+  // Holders of each key attribute, in relation order.
+  std::map<std::string, std::vector<int>> holders;
   for (int i = 0; i < r; ++i)
-    for (const auto& a : nodes[i]->key_names) attr_nodes[a].push_back(i);
-  for (const auto& [attr, ns] : attr_nodes) {
-    if (ns.size() < 2)
-      fail(FG_E_TREE, "key attribute '" + attr + "' of relation " +
-                          nodes[ns[0]]->name +
+    for (const auto& k : nodes[i]->key_names) holders[k].push_back(i);
+  for (const auto& entry : holders) {
+    const std::string& attr = entry.first;
+    const std::vector<int>& hs = entry.second;
+    if (hs.size() == 1)
+      fail(FG_E_TREE, "key attribute '" + attr + "' of relation " + nodes[hs[0]]->name +
                           " is not shared with any other relation");
-    for (size_t x = 0; x < ns.size(); ++x)
-      for (size_t y = x + 1; y < ns.size(); ++y)
-        for (int n : path_between(ns[x], ns[y])) {
-          const auto& ks = nodes[n]->key_names;
-          if (std::find(ks.begin(), ks.end(), attr) == ks.end())
-            fail(FG_E_TREE, "path property violated for attribute '" + attr +
-                                "': relation " + nodes[n]->name +
-                                " does not contain it");
-        }
+    // Connected holders <=> (#holders - 1) tree edges between holders; only
+    // a disconnected set needs the pairwise search for the reported relation.
+    int edges = 0;
+    for (int h : hs)
+      if (nodes[h]->parent != -1 && has[nodes[h]->parent].count(attr)) ++edges;
+    if (edges == (int)hs.size() - 1) continue;
+    for (size_t i = 0; i < hs.size(); ++i)
+      for (size_t j = i + 1; j < hs.size(); ++j) {
+        const int gap = first_gap(hs[i], hs[j], attr);
+        if (gap >= 0)
+          fail(FG_E_TREE, "path property violated for attribute '" + attr + "': relation " +
+                              nodes[gap]->name + " does not contain it");
+      }
   }
-  std::map<std::string, int> data_owner;
+  // Data attribute names: one owner each, never a key attribute anywhere.
+  std::map<std::string, int> owner;
   for (int i = 0; i < r; ++i)
-    for (const auto& a : nodes[i]->data_names) {
-      auto [it, fresh] = data_owner.emplace(a, i);
-      if (!fresh)
-        fail(FG_E_SCHEMA, "data attribute '" + a + "' appears in both " +
-                              nodes[it->second]->name + " and " +
-                              nodes[i]->name);
-      if (attr_nodes.count(a))
-        fail(FG_E_SCHEMA, "attribute '" + a + "' is a data column of " +
-                              nodes[i]->name + " but a key column elsewhere");
+    for (const auto& d : nodes[i]->data_names) {
+      const auto ins = owner.insert({d, i});
+      if (!ins.second)
+        fail(FG_E_SCHEMA, "data attribute '" + d + "' appears in both " +
+                              nodes[ins.first->second]->name + " and " + nodes[i]->name);
+      if (holders.count(d))
+        fail(FG_E_SCHEMA, "attribute '" + d + "' is a data column of " + nodes[i]->name +
+                              " but a key column elsewhere");
     }
 }
 

@@ -31,55 +31,65 @@ void launch_pack_keys(Context& ctx, const int64_t* keys, int64_t rows,
 // Re-packs already packed keys into another field layout (projection).
 void launch_project(Context& ctx, const uint64_t* in, int64_t n,
                     const PackSpec& from_to, uint64_t* out);
-// Stable radix sort of (key, perm) on the low `bits` bits + run-length
-// grouping.  perm_in is overwritten.  Returns G (host; synchronises).
+// Stable radix sort of (key, perm) on the low `bits` bits + segment
+// extraction.  perm_in == null means the identity permutation.
 struct GroupOut {
   DevArray<int> perm;       // n
-  DevArray<int> begins;     // G + 1
-  DevArray<uint64_t> uniq;  // G
-  DevArray<uint64_t> sorted;  // n (only with keep_sorted)
+  DevArray<int> begins;     // G + 1 (allocated with n + 1 entries)
+  DevArray<uint64_t> uniq;  // G (allocated with n entries)
   int64_t G = 0;
 };
+// Returns G on the host (synchronises).
 void group_sorted(Context& ctx, const uint64_t* keys, int64_t n, int bits,
-                  const int* perm_in, GroupOut& out, bool keep_sorted = false);
-// Split form: begin (sort + run-length, no sync) for several inputs, one
-// sync reading every pend.nr, then finish with the counts.
+                  const int* perm_in, GroupOut& out);
+void group_sorted32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
+                    const int* perm_in, GroupOut& out);
+// Split form: begin (sort + segments, no sync) for several inputs, one sync
+// reading every pend.nr, then finish with the counts.  `hist` = the digit
+// histograms from launch_pack_hist (null: computed here); `pidx` (optional,
+// n entries) receives the run id of every input element.
 struct GroupPending {
   int64_t n = 0;
-  bool wide = true;
-  bool keep_sorted = false;
-  DevArray<uint64_t> sorted64, uniq64;
-  DevArray<uint32_t> sorted32, uniq32;
-  DevArray<int> counts;
+  DevArray<int> begins;
+  DevArray<uint64_t> uniq;
   DevArray<int64_t> nr;  // device: number of runs
 };
 void group_begin(Context& ctx, const uint64_t* keys, int64_t n, int bits,
-                 const int* perm_in, GroupOut& out, GroupPending& pend);
+                 const int* perm_in, GroupOut& out, GroupPending& pend,
+                 const uint32_t* hist = nullptr, int* pidx = nullptr);
 void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
-                   const int* perm_in, GroupOut& out, GroupPending& pend);
+                   const int* perm_in, GroupOut& out, GroupPending& pend,
+                   const uint32_t* hist = nullptr, int* pidx = nullptr);
 void group_finish(Context& ctx, int64_t G, GroupOut& out, GroupPending& pend);
 // Same for keys already in ascending order (no sort; perm_in is kept).
 void group_begin_presorted(Context& ctx, const uint64_t* keys, int64_t n,
-                           const int* perm_in, GroupOut& out, GroupPending& pend);
-// Same with 32-bit packed keys (own keys of <= 32 significant bits).
-void group_sorted32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
-                    const int* perm_in, GroupOut& out, bool keep_sorted = false);
-// Without syncing: sort only (keys_out/perm_out) -- used when the caller
-// batches syncs itself.
-template <class KeyT>
-void sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out,
-                const int* vals_in, int* vals_out, int64_t n, int bits);
-// Run-length encode a sorted key array. Writes uniq, counts and *num_runs
-// (device); no sync.
-template <class KeyT>
-void run_length(Context& ctx, const KeyT* sorted, int64_t n,
-                KeyT* uniq, int* counts, int64_t* num_runs_dev);
+                           const int* perm_in, GroupOut& out, GroupPending& pend,
+                           int* pidx = nullptr);
 void exclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
 void inclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
-// pidx[perm[s]] = run id of sorted position s.
-void launch_run_ids(Context& ctx, const uint64_t* sorted, const int* perm,
-                    int64_t n, int* scratch_flags, int* scratch_scan,
-                    int* pidx);
+
+// ---- radix.cu ---------------------------------------------------------------
+// Entries of the digit-histogram buffer of a `bits`-bit sort.
+size_t radix_hist_size(int bits);
+int radix_passes(int bits);
+// Key packing fused with the digit histograms of the sort that follows.
+template <class KeyT>
+void launch_pack_hist(Context& ctx, const int64_t* keys, int64_t rows, int n_key,
+                      const PackSpec& spec, int bits, KeyT* out, uint32_t* hist);
+// Stable LSD onesweep sort of (key, val); vals_in == null sorts row ids.
+template <class KeyT>
+void radix_sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out, const int* vals_in,
+                      int* vals_out, int64_t n, int bits, const uint32_t* hist = nullptr);
+// Runs of a sorted key array: begins[0..G] (begins[G] = n), uniq[0..G),
+// *n_runs = G (device); pidx[perm ? perm[p] : p] = run of position p.
+template <class KeyT>
+void launch_segments(Context& ctx, const KeyT* sorted, int64_t n, int* begins, uint64_t* uniq,
+                     int64_t* n_runs, const int* perm, int* pidx);
+void scan_int(Context& ctx, const int* in, int* out, int64_t n, bool inclusive);
+// out[0..*count) = in[i] for keep[i] != 0, in order (device count).
+void compact_flagged(Context& ctx, const int* in, const char* keep, int* out, int64_t n,
+                     int64_t* count);
+
 // For each of n packed keys (projected to the child's parent-key layout by
 // `proj`), binary search it in sorted `table` (size m); write the index or
 // flag ST_MISSING_CHILD and write -1.
@@ -95,6 +105,8 @@ void launch_lookup_bits(Context& ctx, const uint64_t* own_keys, int64_t n,
 void launch_unpack(Context& ctx, const uint64_t* in, int64_t n,
                    const PackSpec& spec, int64_t* out);
 void launch_iota(Context& ctx, int* out, int64_t n);
+// out[i] = low 32 bits of in[i].
+void launch_narrow(Context& ctx, const uint64_t* in, int64_t n, uint32_t* out);
 // counts[g] = begins[g+1] - begins[g]
 void launch_seg_sizes(Context& ctx, const int* begins, int64_t G,
                       uint64_t* sizes);

@@ -22,8 +22,6 @@
 #include <string>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_select.cuh>
 
 #include "host_tree.hpp"
 #include "launchers.cuh"
@@ -155,15 +153,9 @@ void semi_join(Context& ctx, NodeState& a, NodeState& b,
   if (b.rows) {
     int bits = 0;
     for (int x : attrs) bits += code[x].bits;
-    size_t temp = 0;
-    FG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, qb.get(), tb.get(),
-                                           b.rows, 0, std::max(bits, 1),
-                                           ctx.stream));
-    DevArray<unsigned char> tmp(temp, ctx.stream);
-    FG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), temp, qb.get(), tb.get(),
-                                           b.rows, 0, std::max(bits, 1),
-                                           ctx.stream));
-    ctx.launches += 3;
+    DevArray<int> tv(b.rows, ctx.stream);
+    radix_sort_pairs<uint64_t>(ctx, qb.get(), tb.get(), nullptr, tv.get(), b.rows,
+                               std::max(bits, 1));
   }
   DevArray<char> keep(a.rows, ctx.stream);
   if (a.rows) {
@@ -181,15 +173,7 @@ void semi_join(Context& ctx, NodeState& a, NodeState& b,
   }
   DevArray<int> next(a.rows, ctx.stream);
   DevArray<int64_t> nsel(1, ctx.stream);
-  size_t temp = 0;
-  FG_CUDA(cub::DeviceSelect::Flagged(nullptr, temp, cur.get(), keep.get(),
-                                     next.get(), nsel.get(), a.rows,
-                                     ctx.stream));
-  DevArray<unsigned char> tmp(temp, ctx.stream);
-  FG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), temp, cur.get(), keep.get(),
-                                     next.get(), nsel.get(), a.rows,
-                                     ctx.stream));
-  ctx.launches += 2;
+  compact_flagged(ctx, cur.get(), keep.get(), next.get(), a.rows, nsel.get());
   int64_t m = 0;
   FG_CUDA(cudaMemcpyAsync(&m, nsel.get(), sizeof m, cudaMemcpyDeviceToHost,
                           ctx.stream));
@@ -423,7 +407,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   std::vector<GroupPending> pend(nodes.size());
   std::vector<DevArray<uint32_t>> pk32(nodes.size());
   std::vector<DevArray<uint64_t>> pk64(nodes.size());
-  std::vector<DevArray<int>> iotas(nodes.size());
+  std::vector<DevArray<uint32_t>> hists(nodes.size());
   for (size_t ni = 0; ni < nodes.size(); ++ni) {
     NodeState& n = *nodes[ni];
     n.own = make_spec(n.key_attr, code,
@@ -433,31 +417,32 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
                                      n.key_attr.begin());
                       },
                       &n.own_bits, "relation " + n.name);
+    hists[ni].alloc(radix_hist_size(n.own_bits), st);
     if (n.own_bits <= 32 && !n.has_sel) {
       // Narrow packed keys: 8 instead of 12 bytes per element per radix pass.
+      // Packing also builds every pass's digit histogram; the first pass
+      // generates the row ids itself.
       pk32[ni].alloc(n.rows, st);
-      iotas[ni].alloc(n.rows, st);
-      launch_pack_keys<uint32_t>(ctx, n.keys, n.rows, n.n_key, n.own, pk32[ni].get(),
-                                 iotas[ni].get());
-      group_begin32(ctx, pk32[ni].get(), n.rows, n.own_bits, iotas[ni].get(), n.grp,
-                    pend[ni]);
+      launch_pack_hist<uint32_t>(ctx, n.keys, n.rows, n.n_key, n.own, n.own_bits,
+                                 pk32[ni].get(), hists[ni].get());
+      group_begin32(ctx, pk32[ni].get(), n.rows, n.own_bits, nullptr, n.grp, pend[ni],
+                    hists[ni].get());
+    } else if (!n.has_sel) {
+      pk64[ni].alloc(n.rows, st);
+      launch_pack_hist<uint64_t>(ctx, n.keys, n.rows, n.n_key, n.own, n.own_bits,
+                                 pk64[ni].get(), hists[ni].get());
+      group_begin(ctx, pk64[ni].get(), n.rows, n.own_bits, nullptr, n.grp, pend[ni],
+                  hists[ni].get());
     } else {
       pk64[ni].alloc(n.rows, st);
       if (n.rows) {
-        if (n.has_sel) {
-          k_pack_sel<<<grid1d(ctx, n.rows), 256, 0, st>>>(n.keys, n.n_key,
-                                                          n.sel.get(), n.rows,
-                                                          n.own, pk64[ni].get());
-          FG_LAUNCHED(ctx);
-          FG_KERNEL_CHECK();
-        } else {
-          iotas[ni].alloc(n.rows, st);
-          launch_pack_keys<uint64_t>(ctx, n.keys, n.rows, n.n_key, n.own,
-                                     pk64[ni].get(), iotas[ni].get());
-        }
+        k_pack_sel<<<grid1d(ctx, n.rows), 256, 0, st>>>(n.keys, n.n_key,
+                                                        n.sel.get(), n.rows,
+                                                        n.own, pk64[ni].get());
+        FG_LAUNCHED(ctx);
+        FG_KERNEL_CHECK();
       }
-      group_begin(ctx, pk64[ni].get(), n.rows, n.own_bits,
-                  n.has_sel ? n.sel.get() : iotas[ni].get(), n.grp, pend[ni]);
+      group_begin(ctx, pk64[ni].get(), n.rows, n.own_bits, n.sel.get(), n.grp, pend[ni]);
     }
   }
   {
@@ -471,7 +456,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       group_finish(ctx, Gs[ni], n.grp, pend[ni]);
       pk32[ni].release();
       pk64[ni].release();
-      iotas[ni].release();
+      hists[ni].release();
       n.sizes.alloc(n.grp.G, st);
       launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
     }
@@ -483,7 +468,6 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     std::vector<GroupPending> ppend(nodes.size());
     std::vector<GroupOut> pgs(nodes.size());
     std::vector<DevArray<uint64_t>> ppks(nodes.size());
-    std::vector<DevArray<int>> piotas(nodes.size());
     for (size_t ni = 0; ni < nodes.size(); ++ni) {
       NodeState& n = *nodes[ni];
       if (n.parent < 0) continue;
@@ -499,18 +483,20 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       const int64_t G = n.grp.G;
       ppks[ni].alloc(G, st);
       launch_project(ctx, n.grp.uniq.get(), G, n.par, ppks[ni].get());
-      piotas[ni].alloc(G, st);
-      launch_iota(ctx, piotas[ni].get(), G);
-      ppend[ni].keep_sorted = true;
+      // pidx[g] = parent-key run of own segment g, written by the segment
+      // extraction of the parent-key grouping.
+      n.pidx.alloc(G, st);
       // Parent attributes that are the leading own-key attributes (in the
       // same order) project the ascending own keys to ascending parent
       // keys: no sort needed (C3's F under D1, C4's R2 under R1, 2-way joins).
       const bool prefix = n.pattr.size() <= n.key_attr.size() &&
                           std::equal(n.pattr.begin(), n.pattr.end(), n.key_attr.begin());
       if (prefix)
-        group_begin_presorted(ctx, ppks[ni].get(), G, piotas[ni].get(), pgs[ni], ppend[ni]);
+        group_begin_presorted(ctx, ppks[ni].get(), G, nullptr, pgs[ni], ppend[ni],
+                              n.pidx.get());
       else
-        group_begin(ctx, ppks[ni].get(), G, pbits, piotas[ni].get(), pgs[ni], ppend[ni]);
+        group_begin(ctx, ppks[ni].get(), G, pbits, nullptr, pgs[ni], ppend[ni], nullptr,
+                    n.pidx.get());
     }
     std::vector<int64_t> Ps(nodes.size(), 0);
     bool any = false;
@@ -531,10 +517,6 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       n.pa_perm = std::move(pg.perm);
       n.pa_begins = std::move(pg.begins);
       n.upk = std::move(pg.uniq);
-      n.pidx.alloc(G, st);
-      DevArray<int> flags(G, st), scan(G, st);
-      launch_run_ids(ctx, pg.sorted.get(), n.pa_perm.get(), G, flags.get(),
-                     scan.get(), n.pidx.get());
       if (n.children.empty() && n.P != G)
         fail(FG_E_INTEGRITY, "relation " + n.name +
                                  ": leaf keys do not match its parent attributes");
@@ -620,8 +602,10 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     // by its project-away, which builds them on the fly from the own heads
     // and the children's summaries -- S holds just the heads (C3's fact
     // node: 54 M x 8 instead of 54 M x 20 written, read and re-read).
+    // Measured slower than materialising S (C3: figaro 19.0 -> 27.7 ms; the
+    // per-row factor loads dominate), so it is opt-in (FG_JOIN_ON_READ=1).
     const bool vj = !is_root && !is_leaf && n.width > 0 &&
-                    (int)n.children.size() <= 4 && getenv("FG_NO_JOIN_ON_READ") == nullptr;
+                    (int)n.children.size() <= 4 && getenv("FG_JOIN_ON_READ") != nullptr;
     const int64_t ldS = vj ? n.w : n.width;
     // Every element of S is written: own columns by the heads (one per
     // group), child columns by the join (zero for a missing child), so no
@@ -1119,10 +1103,14 @@ fg_status fg_group_keys(fg_ctx* c, const uint64_t* keys, int64_t n,
     Context& ctx = *reinterpret_cast<Context*>(c);
     if (bits < 0 || bits > 64) fail(FG_E_ARG, "bits out of range");
     if (n > INT_MAX) fail(FG_E_UNSUPPORTED, "more than 2^31-1 keys");
-    fg::DevArray<int> iota(n, ctx.stream);
-    fg::launch_iota(ctx, iota.get(), n);
     fg::GroupOut g;
-    fg::group_sorted(ctx, keys, n, bits, iota.get(), g);
+    if (bits <= 32) {  // the pipeline's narrow-key path (8 bytes per element per pass)
+      fg::DevArray<uint32_t> k32(n, ctx.stream);
+      fg::launch_narrow(ctx, keys, n, k32.get());
+      fg::group_sorted32(ctx, k32.get(), n, bits, nullptr, g);
+    } else {
+      fg::group_sorted(ctx, keys, n, bits, nullptr, g);
+    }
     if (n) {
       FG_CUDA(cudaMemcpyAsync(perm, g.perm.get(), n * sizeof(int),
                               cudaMemcpyDeviceToDevice, ctx.stream));

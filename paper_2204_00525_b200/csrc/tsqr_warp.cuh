@@ -87,6 +87,9 @@ __device__ __forceinline__ Reflector make_reflector_warp(double alpha, double si
 #ifndef FG_NCH
 #define FG_NCH 4
 #endif
+#ifndef FG_ABSORB_OVL
+#define FG_ABSORB_OVL 1
+#endif
 // ROLL_ = 1 keeps only the column-block loop unrolled in absorb_tile (the
 // TC steps inside a block run as a loop): ~1/TC of the code, for kernels
 // whose straight-line body overflows the instruction cache.
@@ -119,10 +122,10 @@ __device__ __forceinline__ double wgroup_sum(double x) {
   return x;
 }
 
-// One column step k of absorb_tile; QB (the column block) is compile-time,
-// the position inside the block may be a run-time value.
+// Sequential form of absorb_step: the dots are reduced after the reflector
+// (u0 * R_kq folded in before the reduction) -- fewer live registers.
 template <class C, int QB, bool REC = false>
-__device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
+__device__ __forceinline__ void absorb_step_seq(double (&X)[C::RPT][C::CPT],
                                             double (&Racc)[C::RR][C::CPT],
                                             int r, int c, const int (&cols)[C::CPT],
                                             int within, double* rec = nullptr) {
@@ -185,6 +188,105 @@ __device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
     for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
     if (r == rk) {
       const double nr = (q == QB && c == ck) ? h.beta : fma(-f, h.u0, rq);
+#pragma unroll
+      for (int m = 0; m < C::RR; ++m)
+        if (mk == m) Racc[m][q] = nr;
+    }
+  }
+}
+
+// One column step k of absorb_tile; QB (the column block) is compile-time,
+// the position inside the block may be a run-time value.
+//
+// Critical path per column: broadcast of column k (RPT shuffles), the
+// squared norm and every trailing dot product x . X_q reduced TOGETHER in
+// one xor tree (independent shuffles, so the latencies overlap), the
+// reflector, and the update.  The pivot-row term u0 * R_kq of each dot
+// (u0 = alpha - beta is known only after the reflector) is added after the
+// reduction from a broadcast of accumulator row k that does not depend on
+// this column's data.
+template <class C, int QB, bool REC = false>
+__device__ __forceinline__ void absorb_step(double (&X)[C::RPT][C::CPT],
+                                            double (&Racc)[C::RR][C::CPT],
+                                            int r, int c, const int (&cols)[C::CPT],
+                                            int within, double* rec = nullptr) {
+  // FG_ABSORB_OVL: 0 sequential everywhere, 1 overlapped everywhere,
+  // 2 overlapped where registers allow (one CTA per SM, MINB == 1).
+  if constexpr (FG_ABSORB_OVL == 0 || (FG_ABSORB_OVL == 2 && C::MINB != 1)) {
+    absorb_step_seq<C, QB, REC>(X, Racc, r, c, cols, within, rec);
+    return;
+  }
+  const int k = QB * C::TC + within;
+  const int ck = (QB & 1) ? C::TC - 1 - within : within;
+  const int rk = k % C::TR;   // lane row holding accumulator row k
+  const int mk = k / C::TR;
+  constexpr int NCH = FG_NCH < C::RPT ? FG_NCH : C::RPT;
+  constexpr int NQ = C::CPT - QB;  // slots holding columns >= the pivot block
+  // Racc[mk][q] for a possibly run-time mk: a select chain over RR rows.
+  auto racc = [&](int q) {
+    double x = Racc[0][q];
+#pragma unroll
+    for (int m = 1; m < C::RR; ++m)
+      if (mk == m) x = Racc[m][q];
+    return x;
+  };
+  // Accumulator row k, slot q, as seen by every lane of column group c.
+  double rk_q[NQ];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) rk_q[j] = __shfl_sync(0xffffffffu, racc(QB + j), rk + c * C::TR);
+  const double alpha = __shfl_sync(0xffffffffu, racc(QB), rk + ck * C::TR);
+  double v[C::RPT];
+  double sa[NCH];
+#pragma unroll
+  for (int i = 0; i < C::RPT; ++i) {
+    v[i] = __shfl_sync(0xffffffffu, X[i][QB], r + ck * C::TR);
+    if (i < NCH) sa[i] = v[i] * v[i];
+    else sa[i % NCH] = fma(v[i], v[i], sa[i % NCH]);
+  }
+  double red[NQ + 1];
+#pragma unroll
+  for (int w = NCH / 2; w; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) sa[i] += sa[i + w];
+  red[NQ] = sa[0];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    double da[NCH];
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i) {
+      if (i < NCH) da[i] = v[i] * X[i][QB + j];
+      else da[i % NCH] = fma(v[i], X[i][QB + j], da[i % NCH]);
+    }
+#pragma unroll
+    for (int w = NCH / 2; w; w >>= 1)
+#pragma unroll
+      for (int i = 0; i < w; ++i) da[i] += da[i + w];
+    red[j] = da[0];
+  }
+#pragma unroll
+  for (int o = C::TR / 2; o; o >>= 1)
+#pragma unroll
+    for (int j = 0; j <= NQ; ++j) red[j] += __shfl_xor_sync(0xffffffffu, red[j], o);
+  const Reflector h = make_reflector_warp(alpha, red[NQ]);
+  if constexpr (REC) {
+    // Reflector k for the caller's block update: {u0, t1, t2}.
+    if ((threadIdx.x & 31) == 0) {
+      rec[3 * k] = h.u0;
+      rec[3 * k + 1] = h.t1;
+      rec[3 * k + 2] = h.t2;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const int q = QB + j;
+    // Slots past the pivot block hold only columns > k.
+    const bool act = q > QB || cols[q] > k;
+    const double dsum = fma(h.u0, rk_q[j], red[j]);
+    const double f = act ? (dsum * h.t1) * h.t2 : 0.0;
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i) X[i][q] = fma(-f, v[i], X[i][q]);
+    if (r == rk) {
+      const double nr = (q == QB && c == ck) ? h.beta : fma(-f, h.u0, rk_q[j]);
 #pragma unroll
       for (int m = 0; m < C::RR; ++m)
         if (mk == m) Racc[m][q] = nr;

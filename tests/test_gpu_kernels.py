@@ -26,7 +26,15 @@ def dev(x):
 
 
 @pytest.mark.parametrize("n,bits,hi", [(1, 0, 1), (1000, 10, 1000), (100_000, 17, 100_000),
-                                       (300_000, 40, 1 << 40), (50_000, 64, None), (0, 5, 1)])
+                                       (300_000, 40, 1 << 40), (50_000, 64, None), (0, 5, 1),
+                                       # onesweep tile edges (4096 u64 / 6144 u32 keys per tile)
+                                       (4096, 33, 1 << 33), (4097, 33, 1 << 33), (6144, 12, 7),
+                                       (6145, 20, 1 << 20), (12_289, 9, 512),
+                                       # all keys equal with bits > 0; one-bit keys
+                                       (20_000, 16, 1), (30_000, 1, 2),
+                                       # 7+7+6-bit passes (C2's 20-bit keys), 8x6 passes (C3)
+                                       (2_000_003, 20, 1 << 20), (1_500_000, 47, 1 << 47),
+                                       (1_000_000, 32, 1 << 32), (700_000, 63, 1 << 63)])
 def test_group_keys_stable(n, bits, hi):
     rng = np.random.default_rng(n + bits)
     if hi is None:
@@ -148,3 +156,20 @@ def test_tsqr_wide_large_spans(w):
     Rk = F.tsqr([(dev(xr), 0)], len(keep)).cpu().numpy()
     ref = fo.normalize_signs(np.linalg.qr(xr, mode="r"))
     assert r_distance(Rk, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("bits", [20, 47])
+def test_group_keys_zipf(bits):
+    """Heavily skewed keys (Zipf 1.1 / 1.3, as C3's fact keys and C5) through
+    the onesweep sort: stable permutation and offsets bit-exact."""
+    rng = np.random.default_rng(bits)
+    n = 3_000_000
+    z = rng.zipf(1.1 if bits > 32 else 1.3, n) % (1 << min(bits, 40))
+    keys = (z.astype(np.uint64) * np.uint64(2654435761)) & np.uint64((1 << bits) - 1)
+    perm, begins, uniq = F.group_keys(dev(keys.view(np.int64)), bits)
+    ref_perm = np.argsort(keys, kind="stable")
+    assert np.array_equal(perm.cpu().numpy(), ref_perm.astype(np.int32))
+    sk = keys[ref_perm]
+    u, first = np.unique(sk, return_index=True)
+    assert np.array_equal(uniq.cpu().numpy().view(np.uint64), u)
+    assert np.array_equal(begins.cpu().numpy(), np.append(first, n).astype(np.int32))

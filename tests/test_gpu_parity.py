@@ -198,6 +198,14 @@ def test_errors_match_reference_taxonomy():
     db = fgdb.Database([mk("S", ["X"], ["a"], k(1), d(1)), mk("T", ["X"], ["a"], k(1), d(1))], 0, [-1, 0])
     with pytest.raises(F.schema_error):
         run_gpu(db)
+    # path property (join_tree.hpp:120-153): X held by S and V but not by the
+    # relation between them; the reported relation is the reference's (the
+    # first holder pair, first gap along the tree path).
+    kk = lambda n: np.ones((1, n), dtype=np.int64)  # noqa: E731
+    db = fgdb.Database([mk("S", ["X", "Y"], ["a"], kk(2), d(1)), mk("U", ["Y", "Z"], ["b"], kk(2), d(1)),
+                        mk("V", ["X", "Z"], ["c"], kk(2), d(1))], 0, [-1, 0, 1])
+    with pytest.raises(F.tree_error, match="relation U does not contain it"):
+        run_gpu(db)
 
 
 @pytest.mark.parametrize("cfg,scale", [("C5", 0.003), ("C2", 0.05), ("C3", 0.002),
