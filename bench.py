@@ -213,12 +213,22 @@ def device_relations(db, F, torch):
 class Runner:
     """One database on the device; step() = one pipeline (+ gather/merge)."""
 
-    def __init__(self, db, F, D, torch, local, world, presorted=False):
+    def __init__(self, db, F, D, torch, local, world, presorted=False, plan=None, heavy=None):
         self.F, self.D, self.torch, self.local, self.world = F, D, torch, local, world
         self.rels = device_relations(db, F, torch)
         self.tree = F.build_join_tree(self.rels, db.root, db.parent)
-        self.opts = F.PipelineOptions(assume_reduced=True)
-        self.rows = sum(r.rows for r in db.relations)
+        self.root = db.root
+        self.n = sum(len(r.data_attrs) for r in db.relations)
+        # Strong scaling: the partition plan and this rank's heavy-key rows
+        # (device-resident); shards with replicated rows need reduction.
+        self.plan = plan
+        self.heavy = None
+        if heavy is not None:
+            self.heavy = [(k, torch.from_numpy(d).cuda()) for k, d in heavy]
+        reduced = plan is None or not plan.needs_reduction(db.relations)
+        self.opts = F.PipelineOptions(assume_reduced=reduced)
+        self.rows = sum(r.rows for r in db.relations) + \
+            sum(int(k.shape[0]) for k, _ in (heavy or []))
         self.gather_s = 0.0
         if presorted:
             # Paper convention (PAPER.md:951-954): relations already sorted by
@@ -230,6 +240,17 @@ class Runner:
                                           r.keys[perm].contiguous(), r.data[perm].contiguous())
 
     def step(self):
+        if self.plan is not None and self.world > 1:
+            # Strong scaling: the whole per-rank flow of distributed.py
+            # (pipeline on the shard, heavy-key stage, gathers, merge).
+            out = []
+            g0 = time.perf_counter()
+            R = self.D.distributed_factor(self.rels, self.heavy, self.tree, self.n, self.plan,
+                                          self.root, device=self.local,
+                                          assume_reduced=self.opts.assume_reduced, results=out)
+            self.torch.cuda.synchronize()
+            self.gather_s += time.perf_counter() - g0
+            return (out[0] if out else _EmptyResult()), R
         res = self.F.run_pipeline(self.rels, self.tree, self.opts, device=self.local,
                                   fetch_counts=False)
         R = res.factor.r
@@ -289,6 +310,14 @@ class Runner:
         return ms, {k: (v / steps if isinstance(v, float) else v) for k, v in acc.items()}
 
 
+class _EmptyResult:
+    """Phase counters of a rank whose shard join was empty."""
+    seconds_group = seconds_counts = seconds_figaro = seconds_postprocess = 0.0
+    seconds_headtail_kernels = seconds_tsqr_kernels = headtail_bytes = 0.0
+    headtail_fused_flops = tsqr_stage_flops = 0.0
+    headtail_launches = fused_launches = host_syncs = 0
+
+
 class _Null:
     def __enter__(self):
         return self
@@ -338,6 +367,9 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-side collectives, for checking the N>1 flow with "
+                         "ranks sharing one GPU (no rank waits on another's kernels)")
     ap.add_argument("--ref-scale", type=float, default=None,
                     help="reference-arm scale relative to --scale (default REF_SCALE[config])")
     ap.add_argument("--ref-budget", type=float, default=150.0,
@@ -361,25 +393,38 @@ def main():
     from paper_2204_00525_b200 import figaro as F
     from paper_2204_00525_b200 import workloads
 
+    if args.dist_backend == "gloo":  # ranks may share a GPU
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     stream = torch.cuda.current_stream()
     ctx = F.get_context(local)
     ctx.bind_current_stream()
     dd = dist if world > 1 else None
 
+    plan = heavy = None
     if world > 1 and args.scaling == "strong":
-        db = D.shard_database(workloads.make(args.config, seed=args.seed, scale=args.scale),
-                              rank, world)
+        # One global database through the partition plan (distributed.py).
+        full = workloads.make(args.config, seed=args.seed, scale=args.scale)
+        plan = D.plan_partition(full.relations, full.root, world, parent=full.parent)
+        db = D.shard_database(full, rank, world, plan)
+        heavy = D.heavy_rows(full.relations, plan, rank) if plan.combine else None
+        global_rows = workloads.input_rows(full)
+        del full
     else:
         db = D.weak_shard(workloads.make(args.config, seed=args.seed + 1000003 * rank,
                                          scale=args.scale), rank, world)
-    runner = Runner(db, F, D, torch, local, world)
+    runner = Runner(db, F, D, torch, local, world, plan=plan, heavy=heavy)
     m_rank = runner.rows
     clk = ClockSampler(local)
     ms, acc = runner.timed(args.steps, args.warmup, stream, dd, clocks=clk)
-    if world > 1:
+    if plan is not None:
+        m_total = float(global_rows)  # strong scaling: the one database's tuples
+    elif world > 1:
         t = torch.tensor([m_rank], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
         m_total = float(t.item())
@@ -397,17 +442,28 @@ def main():
         h2d += k.numel() * 8 + d.numel() * 8
         host_rels.append(F.Relation(r.name, r.key_attrs, r.data_attrs, k.numpy(), d.numpy()))
     opts = runner.opts
-    F.run_pipeline(host_rels, runner.tree, opts, device=local, fetch_counts=False)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
+    if heavy is not None:
+        h2d += sum(d.size * 8 for _, d in heavy)
+
+    def e2e_step():
+        if plan is not None:  # strong scaling: the whole distributed flow from host buffers
+            return D.distributed_factor(host_rels, heavy, runner.tree, runner.n, plan,
+                                        runner.root, device=local,
+                                        assume_reduced=opts.assume_reduced).cpu().numpy()
         hr = F.run_pipeline(host_rels, runner.tree, opts, device=local, fetch_counts=False)
         Rh = hr.factor.r
         if world > 1:
             Rh = D.gather_and_merge(torch.from_numpy(Rh).cuda(),
                                     lambda p, n: D.device_merge(p, n, device=local)).cpu().numpy()
+        return Rh
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
@@ -470,7 +526,10 @@ def main():
                        "input_rows": int(m_total), "input_rows_per_gpu": m_rank,
                        "columns": n, "tree": TREES[args.config],
                        "l2": "inputs larger than L2 (no flush)",
-                       "parallelism": f"key-hash x{world}" + (f" ({args.scaling})" if world > 1 else ""),
+                       "parallelism": (f"grid {plan.attrs}x{plan.dims}, {len(plan.combine)} "
+                                       f"combined / {len(plan.heavy)} split heavy keys (strong)"
+                                       if plan is not None else
+                                       f"key-hash x{world}" + (" (weak)" if world > 1 else "")),
                        "reference_scale": args.scale * (args.ref_scale or REF_SCALE[args.config])},
             "phases_ms": {"group": acc["group"] * 1e3, "counts": acc["counts"] * 1e3,
                           "figaro": acc["figaro"] * 1e3, "post": acc["post"] * 1e3,

@@ -8,9 +8,11 @@
 //              phi_up_c[lidx_c[k]] += fjs[k]; circ[k] = fjs[k] / rows[k]
 //              phi_up_c[q] /= phi_down_c[q]                 (counts.hpp:190-219)
 // u64 arithmetic with overflow detection (checked_mul / checked_atomic_add,
-// counts.hpp:47-62) and exact-division checks (exact_div, counts.hpp:64-71)
+// counts.hpp:47-62; sums through split low/high-word tables, add_split) and exact-division checks (exact_div, counts.hpp:64-71)
 // raise bits in the device status word instead of throwing.  Integer adds
 // commute, so the tables are bit-identical for any launch shape.
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "launchers.cuh"
@@ -30,12 +32,48 @@ __device__ __forceinline__ uint64_t mul_chk(uint64_t a, uint64_t b,
   return a * b;
 }
 
-__device__ __forceinline__ void add_chk(uint64_t* slot, uint64_t d,
-                                        unsigned* status) {
-  const unsigned long long old =
-      atomicAdd(reinterpret_cast<unsigned long long*>(slot),
-                static_cast<unsigned long long>(d));
-  if (old + d < old) atomicOr(status, ST_OVERFLOW);
+// Global count tables are accumulated exactly without returning atomics:
+// table[0, P) collects the low 32 bits of every addend and table[P, 2P) the
+// high 32 bits (neither can wrap for < 2^31 addends), both with
+// fire-and-forget reductions (RED); k_finalize / k_up_div then form
+// lo + hi * 2^32 in 128-bit arithmetic and flag sums >= 2^64
+// (checked_atomic_add, counts.hpp:54-62).
+__device__ __forceinline__ void add_split(uint64_t* table, int64_t P, int64_t slot,
+                                          uint64_t d) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(table + slot), d & 0xffffffffull);
+  const unsigned long long h = d >> 32;
+  if (h) atomicAdd(reinterpret_cast<unsigned long long*>(table + P + slot), h);
+}
+
+// lo + hi * 2^32, or ~0 with ST_OVERFLOW when it does not fit 64 bits.
+__device__ __forceinline__ uint64_t combine_split(uint64_t lo, uint64_t hi, unsigned* status) {
+  const uint64_t sum = lo + (hi << 32);
+  if ((hi >> 32) != 0 || sum < lo) {
+    atomicOr(status, ST_OVERFLOW);
+    return ~0ull;
+  }
+  return sum;
+}
+
+// Per-block shared-memory cache in front of a split global table: slot
+// claimed by atomicCAS on the table index (direct-mapped); a collision goes
+// straight to the global table.  Flushed once per block (cache_flush).
+constexpr int kCache = 2048;
+struct SmemCache {
+  int* key;
+  unsigned long long* val;
+  unsigned* st;
+};
+__device__ __forceinline__ void cache_add(const SmemCache& c, uint64_t* table, int64_t P,
+                                          int64_t q, unsigned long long x) {
+  const int slot = (int)(((unsigned)q * 2654435761u) >> 21) & (kCache - 1);
+  const int old = atomicCAS(&c.key[slot], -1, (int)q);
+  if (old == -1 || old == (int)q) {
+    const unsigned long long o = atomicAdd(&c.val[slot], x);
+    if (o + x < o) atomicOr(c.st, ST_OVERFLOW);
+  } else {
+    add_split(table, P, q, x);
+  }
 }
 
 // Warp-aggregated checked add: lanes whose `slot` equals the previous
@@ -43,8 +81,9 @@ __device__ __forceinline__ void add_chk(uint64_t* slot, uint64_t d,
 // run issues one atomic.  Segments are sorted by own key, so targets keyed by
 // a prefix of it arrive in runs.  Integer sums commute: the table values do
 // not depend on the aggregation.
-__device__ __forceinline__ void add_runs(uint64_t* table, int64_t slot, uint64_t v,
-                                         bool live, unsigned* status) {
+__device__ __forceinline__ void add_runs(uint64_t* table, int64_t P, int64_t slot, uint64_t v,
+                                         bool live, unsigned* status,
+                                         const SmemCache* cache = nullptr) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int64_t prev = __shfl_up_sync(full, slot, 1);
@@ -70,7 +109,8 @@ __device__ __forceinline__ void add_runs(uint64_t* table, int64_t slot, uint64_t
   const bool tail = live && (lane == 31 || !next_live || next != slot);
   if (tail) {
     if (ovf) atomicOr(status, ST_OVERFLOW);
-    add_chk(&table[slot], acc, status);
+    if (cache) cache_add(*cache, table, P, slot, acc);
+    else add_split(table, P, slot, acc);
   }
 }
 
@@ -78,8 +118,8 @@ __device__ __forceinline__ void add_runs(uint64_t* table, int64_t slot, uint64_t
 // (__match_any_sync) are summed by a log-depth peer reduction and the lowest
 // lane of each peer set issues one atomic.  Zipf-distributed child keys make
 // many lanes of a warp hit the same hot entry.
-__device__ __forceinline__ void add_peers(uint64_t* table, int slot, uint64_t v, bool live,
-                                          unsigned* status, bool shared_table = false) {
+__device__ __forceinline__ void add_peers(uint64_t* table, int64_t P, int slot, uint64_t v,
+                                          bool live, unsigned* status, bool shared_table = false) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned peers0 = __match_any_sync(full, live ? slot : -1);
@@ -109,15 +149,30 @@ __device__ __forceinline__ void add_peers(uint64_t* table, int slot, uint64_t v,
           atomicAdd(reinterpret_cast<unsigned long long*>(table + slot), x);
       if (old + x < old) atomicOr(status, ST_OVERFLOW);
     } else {
-      add_chk(&table[slot], x, status);
+      add_split(table, P, slot, x);
     }
   }
 }
 
 __global__ void k_theta(const uint64_t* __restrict__ sizes, int64_t G,
                         ChildLinks ch, const int* __restrict__ pidx,
-                        uint64_t* phi_down, uint64_t* __restrict__ theta,
+                        uint64_t* phi_down, int64_t P, uint64_t* __restrict__ theta,
                         unsigned* status) {
+  // Run sums of phi_down go through a per-block cache: a long parent-key
+  // run (C3's most frequent k1 covers 5M F segments) costs one global add
+  // per block instead of one per warp.
+  __shared__ int ckey[kCache];
+  __shared__ unsigned long long cval[kCache];
+  __shared__ unsigned sst;
+  const SmemCache cache{ckey, cval, &sst};
+  if (pidx) {
+    for (int i = threadIdx.x; i < kCache; i += blockDim.x) {
+      ckey[i] = -1;
+      cval[i] = 0ull;
+    }
+    if (threadIdx.x == 0) sst = 0;
+    __syncthreads();
+  }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t Gw = (G + 31) & ~int64_t(31);  // warp-uniform trip count
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < Gw; k += stride) {
@@ -136,7 +191,13 @@ __global__ void k_theta(const uint64_t* __restrict__ sizes, int64_t G,
       }
       theta[k] = t;
     }
-    if (pidx) add_runs(phi_down, live ? pidx[k] : -1, t, live, status);
+    if (pidx) add_runs(phi_down, P, live ? pidx[k] : -1, t, live, status, &cache);
+  }
+  if (pidx) {
+    __syncthreads();
+    if (threadIdx.x == 0 && sst) atomicOr(status, sst);
+    for (int i = threadIdx.x; i < kCache; i += blockDim.x)
+      if (ckey[i] >= 0 && cval[i]) add_split(phi_down, P, ckey[i], cval[i]);
   }
 }
 
@@ -175,7 +236,7 @@ __global__ void k_fjs(const uint64_t* __restrict__ sizes,
     }
     for (int c = 0; c < ch.n; ++c) {
       const int q = live ? ch.lidx[c][k] : -1;
-      add_peers(ch.phi_up[c], q, f, live && q >= 0, status);
+      add_peers(ch.phi_up[c], ch.P[c], q, f, live && q >= 0, status);
     }
   }
 }
@@ -184,25 +245,91 @@ __global__ void k_fjs(const uint64_t* __restrict__ sizes,
 // per-block shared-memory copy: contention stays on-chip (C3's D3 has 1,000
 // keys for 54M F segments).
 constexpr int kPrivMax = 4096;  // 32 KB of static shared memory
-__global__ void k_scatter_priv(const uint64_t* __restrict__ fjs, int64_t G,
-                               const int* __restrict__ lidx, uint64_t* table,
-                               int P, unsigned* status) {
-  __shared__ unsigned long long loc[kPrivMax];
+// Scatter-add of fjs into a child table through shared memory.  PRIV: the
+// whole table (P <= kPrivMax) is privatised per block; otherwise a
+// direct-mapped cache of kCache slots claimed by atomicCAS, collisions going
+// to the split global table.  PEERS: warp-aggregate equal targets first
+// (__match_any_sync + log-depth peer sums); without it every element is one
+// shared-memory atomic (hardware-serialised on equal addresses) -- cheaper
+// when a warp's targets repeat only a few times.  Four elements per thread
+// are loaded before the atomics.
+template <bool PRIV, bool PEERS>
+__global__ void __launch_bounds__(256) k_scatter_smem(const uint64_t* __restrict__ fjs, int64_t G,
+                                                      const int* __restrict__ lidx,
+                                                      uint64_t* table, int64_t P,
+                                                      unsigned* status) {
+  constexpr int kSlots = PRIV ? kPrivMax : kCache;
+  __shared__ int ckey[PRIV ? 1 : kSlots];
+  __shared__ unsigned long long cval[kSlots];
   __shared__ unsigned sst;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) loc[i] = 0ull;
+  const SmemCache cache{ckey, cval, &sst};
+  for (int i = threadIdx.x; i < kSlots; i += blockDim.x) {
+    if (!PRIV) ckey[i] = -1;
+    cval[i] = 0ull;
+  }
   if (threadIdx.x == 0) sst = 0;
   __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t Gw = (G + 31) & ~int64_t(31);  // warp-uniform trip count
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < Gw;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int q = k < G ? lidx[k] : -1;
-    const uint64_t v = q >= 0 ? fjs[k] : 0ull;
-    add_peers(reinterpret_cast<uint64_t*>(loc), q, v, q >= 0, &sst, true);
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k0 < Gw; k0 += 4 * stride) {
+    int q[4];
+    uint64_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = k0 + u * stride;
+      q[u] = k < G ? lidx[k] : -1;
+      v[u] = q[u] >= 0 ? fjs[k] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (PEERS) {
+        if (k0 + u * stride >= Gw) continue;  // warp-uniform
+        if (PRIV) add_peers(reinterpret_cast<uint64_t*>(cval), 0, q[u], v[u], q[u] >= 0, &sst, true);
+        else {
+          const unsigned full = 0xffffffffu;
+          const int lane = threadIdx.x & 31;
+          const unsigned peers0 = __match_any_sync(full, q[u]);
+          unsigned long long x = v[u];
+          int ovf = 0;
+          int rel = __popc(peers0 & ((1u << lane) - 1u));
+          unsigned peers = lane == 31 ? 0u : peers0 & ~((2u << lane) - 1u);
+          while (__any_sync(full, peers != 0)) {
+            const int nx = __ffs(peers);
+            const unsigned long long t = __shfl_sync(full, x, nx ? nx - 1 : lane);
+            const int to = __shfl_sync(full, ovf, nx ? nx - 1 : lane);
+            if ((rel & 1) == 0 && nx) {
+              const unsigned long long s2 = x + t;
+              if (s2 < x) ovf = 1;
+              x = s2;
+              ovf |= to;
+            }
+            peers &= ~__ballot_sync(full, rel & 1);
+            rel >>= 1;
+          }
+          if (q[u] >= 0 && lane == __ffs(peers0) - 1) {
+            if (ovf) atomicOr(&sst, ST_OVERFLOW);
+            cache_add(cache, table, P, q[u], x);
+          }
+        }
+      } else if (q[u] >= 0) {
+        if (PRIV) {
+          const unsigned long long o = atomicAdd(&cval[q[u]], v[u]);
+          if (o + v[u] < o) atomicOr(&sst, ST_OVERFLOW);
+        } else {
+          cache_add(cache, table, P, q[u], v[u]);
+        }
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0 && sst) atomicOr(status, sst);
-  for (int i = threadIdx.x; i < P; i += blockDim.x)
-    if (loc[i]) add_chk(&table[i], loc[i], status);
+  for (int i = threadIdx.x; i < (PRIV ? (int)P : kSlots); i += blockDim.x) {
+    if (PRIV) {
+      if (cval[i]) add_split(table, P, i, cval[i]);
+    } else if (ckey[i] >= 0 && cval[i]) {
+      add_split(table, P, ckey[i], cval[i]);
+    }
+  }
 }
 
 __global__ void k_up_div(uint64_t* __restrict__ phi_up,
@@ -210,7 +337,7 @@ __global__ void k_up_div(uint64_t* __restrict__ phi_up,
                          unsigned* status) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P;
        q += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t u = phi_up[q];
+    const uint64_t u = combine_split(phi_up[q], phi_up[P + q], status);
     const uint64_t d = phi_down[q];
     if (u == 0) {
       // The parent never produced this key: counts.hpp:211-214.
@@ -226,6 +353,13 @@ __global__ void k_up_div(uint64_t* __restrict__ phi_up,
   }
 }
 
+// Final values of a split table (see add_split).
+__global__ void k_finalize(uint64_t* __restrict__ table, int64_t P, unsigned* status) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P;
+       q += (int64_t)gridDim.x * blockDim.x)
+    table[q] = combine_split(table[q], table[P + q], status);
+}
+
 inline int grid_for(const Context& ctx, int64_t n) {
   int64_t g = ceil_div(n, kThreads);
   const int64_t cap = static_cast<int64_t>(ctx.sm_count) * 8;
@@ -235,13 +369,18 @@ inline int grid_for(const Context& ctx, int64_t n) {
 }  // namespace
 
 void launch_theta(Context& ctx, const uint64_t* sizes, int64_t G,
-                  const ChildLinks& ch, const int* pidx, uint64_t* phi_down,
+                  const ChildLinks& ch, const int* pidx, uint64_t* phi_down, int64_t P,
                   uint64_t* theta, unsigned* status) {
   if (G == 0) return;
   k_theta<<<grid_for(ctx, G), kThreads, 0, ctx.stream>>>(sizes, G, ch, pidx,
-                                                         phi_down, theta, status);
+                                                         phi_down, P, theta, status);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
+  if (pidx && P > 0) {
+    k_finalize<<<grid_for(ctx, P), kThreads, 0, ctx.stream>>>(phi_down, P, status);
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+  }
 }
 
 void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
@@ -249,15 +388,22 @@ void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
                 const ChildLinks& ch, const int64_t* child_P, uint64_t* fjs,
                 uint64_t* circ, unsigned* status) {
   if (G == 0) return;
+  // Children whose table fits shared memory: full privatisation; children
+  // with many more segments than keys: the shared-memory cache; others
+  // (few segments per key, little contention): warp-aggregated atomics
+  // inside k_fjs.
   ChildLinks big{};
-  std::vector<int> small;
+  std::vector<int> small, cached;
   for (int c = 0; c < ch.n; ++c) {
     if (child_P[c] <= kPrivMax && G > 4 * child_P[c]) {
       small.push_back(c);
+    } else if (G > 16 * child_P[c] && getenv("FG_NO_COUNT_CACHE") == nullptr) {
+      cached.push_back(c);
     } else {
       big.lidx[big.n] = ch.lidx[c];
       big.phi_down[big.n] = ch.phi_down[c];
       big.phi_up[big.n] = ch.phi_up[c];
+      big.P[big.n] = ch.P[c];
       ++big.n;
     }
   }
@@ -266,13 +412,26 @@ void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
                                                        status);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
-  for (int c : small) {
-    const int grid = (int)std::min<int64_t>(ctx.sm_count * 2, ceil_div(G, kThreads));
-    k_scatter_priv<<<std::max(grid, 1), kThreads, 0, ctx.stream>>>(
-        fjs, G, ch.lidx[c], ch.phi_up[c], (int)child_P[c], status);
+  // Measured on C3 (54M F segments): the privatised D3 table (1k keys) is
+  // fastest with plain shared-memory atomics (0.56 vs 0.88 ms), the cached
+  // D2 table (100k Zipf keys) needs the warp aggregation (1.9 vs 6.7 ms).
+  // FG_COUNT_SCATTER=peers|direct forces one form for both.
+  static const int mode = [] {
+    const char* e = getenv("FG_COUNT_SCATTER");
+    if (!e) return 0;
+    return std::string(e) == "peers" ? 1 : 2;
+  }();
+  auto launch = [&](auto kern, int c) {
+    const int grid = (int)std::min<int64_t>(ctx.sm_count * 4, ceil_div(G, kThreads));
+    kern<<<std::max(grid, 1), kThreads, 0, ctx.stream>>>(fjs, G, ch.lidx[c], ch.phi_up[c],
+                                                          child_P[c], status);
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
-  }
+  };
+  for (int c : cached)
+    mode != 2 ? launch(k_scatter_smem<false, true>, c) : launch(k_scatter_smem<false, false>, c);
+  for (int c : small)
+    mode == 1 ? launch(k_scatter_smem<true, true>, c) : launch(k_scatter_smem<true, false>, c);
 }
 
 void launch_up_div(Context& ctx, uint64_t* phi_up, const uint64_t* phi_down,

@@ -27,29 +27,48 @@ inline int grid_for(const Context& ctx, int64_t n, int per_sm = 8) {
 }
 
 // Min/max of every key column in one pass over the row-major key tuples
-// (grid-stride over rows; per-column warp reduction, then atomics).
+// (grid-stride over rows, NK columns known at compile time for the common
+// widths, four rows in flight per thread; per-column warp reduction, then
+// atomics).  NK = 0: any width up to kMaxKeyCols, one row at a time.
+template <int NK>
 __global__ void k_key_minmax(const int64_t* __restrict__ keys, int64_t rows,
                              int n_key, const int* __restrict__ attr_of_col,
                              long long* mins, long long* maxs) {
-  long long lo[kMaxKeyCols], hi[kMaxKeyCols];
+  constexpr int C = NK ? NK : kMaxKeyCols;
+  constexpr int U = NK ? 4 : 1;
+  long long lo[C], hi[C];
 #pragma unroll
-  for (int c = 0; c < kMaxKeyCols; ++c) {
+  for (int c = 0; c < C; ++c) {
     lo[c] = LLONG_MAX;
     hi[c] = LLONG_MIN;
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int nk = NK ? NK : n_key;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < rows; i0 += U * stride) {
+    long long v[U][C];
 #pragma unroll
-    for (int c = 0; c < kMaxKeyCols; ++c) {
-      if (c >= n_key) break;
-      const long long v = keys[i * n_key + c];
-      lo[c] = v < lo[c] ? v : lo[c];
-      hi[c] = v > hi[c] ? v : hi[c];
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        v[u][c] = 0;
+        if (c < nk && i < rows) v[u][c] = keys[i * nk + c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i0 + u * stride >= rows) continue;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (c >= nk) continue;
+        lo[c] = v[u][c] < lo[c] ? v[u][c] : lo[c];
+        hi[c] = v[u][c] > hi[c] ? v[u][c] : hi[c];
+      }
     }
   }
 #pragma unroll
-  for (int c = 0; c < kMaxKeyCols; ++c) {
-    if (c >= n_key) break;
+  for (int c = 0; c < C; ++c) {
+    if (c >= nk) break;
     long long a = lo[c], b = hi[c];
     for (int o = 16; o; o >>= 1) {
       const long long x = __shfl_xor_sync(0xffffffffu, a, o);
@@ -182,8 +201,12 @@ void launch_key_minmax(Context& ctx, const int64_t* keys, int64_t rows,
                        long long* maxs) {
   if (rows == 0 || n_key == 0) return;
   if (n_key > kMaxKeyCols) fail(FG_E_UNSUPPORTED, "more than 16 key columns");
-  k_key_minmax<<<grid_for(ctx, rows, 4), kThreads, 0, ctx.stream>>>(keys, rows, n_key,
-                                                                   attr_of_col_dev, mins, maxs);
+  const int grid = grid_for(ctx, rows, 8);
+  auto kern = n_key == 1 ? k_key_minmax<1>
+            : n_key == 2 ? k_key_minmax<2>
+            : n_key == 3 ? k_key_minmax<3>
+            : n_key == 4 ? k_key_minmax<4> : k_key_minmax<0>;
+  kern<<<grid, kThreads, 0, ctx.stream>>>(keys, rows, n_key, attr_of_col_dev, mins, maxs);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
 }

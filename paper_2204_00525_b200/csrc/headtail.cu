@@ -88,6 +88,16 @@ struct HtDev {
   const double* jscale[kVJMax];
   int jw[kVJMax];
   int joff[kVJMax];
+  // Join-on-write: with wj >= 0 the head emission writes joined summary
+  // rows (own head * prod s_c | child summaries * s_own * prod_{d != c} s_d)
+  // of total width wwidth, and the joined scale into `scales`.
+  int wj;
+  int wwidth;
+  const int* wlidx[kVJMax];
+  const double* wS[kVJMax];
+  const double* wsc[kVJMax];
+  int wcw[kVJMax];
+  int woff[kVJMax];
 };
 
 __device__ __forceinline__ int64_t src_row(const HtDev& a, int64_t p) {
@@ -169,6 +179,7 @@ struct WarpSmemT {
   double buf[CAP];
   double2 coef[kMaxRB];   // {alpha, beta}: tail = a*alpha - S*beta
   double hco[kMaxRB];     // head coefficient at a group's last row
+  double hsc[kMaxRB];     // the group's scale at its last row
   double wt[kMaxRB];      // generalized weights
   int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
   unsigned char startf[kMaxRB];  // 1 where a group starts inside the batch
@@ -250,7 +261,7 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
     }
     __syncwarp();
     const int g = lane / geo.L, cl = lane % geo.L;
-    for (int rr = g; rr < nb; rr += geo.G) {
+    for (int rr = g < geo.G ? g : nb; rr < nb; rr += geo.G) {
       double* dst = sm.buf + rr * geo.ls;
 #pragma unroll
       for (int s = 0; s < SLOTS; ++s) {
@@ -278,7 +289,7 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
     sm.rowptr[rr] = a.data + src_row(a, p + rr) * a.ld;
   __syncwarp();
   const int g = lane / geo.L, cl = lane % geo.L;
-  for (int rr = g; rr < nb; rr += geo.G) {
+  for (int rr = g < geo.G ? g : nb; rr < nb; rr += geo.G) {
     const double* src = sm.rowptr[rr];
     double* dst = sm.buf + rr * geo.ls;
 #pragma unroll
@@ -293,7 +304,7 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
 // F = NoFuse: tails are written to a.tails.  F = WCfg<...>: each batch of
 // tails is written in place into the staged rows (group starts become zero
 // rows) and absorbed into the warp's TSQR accumulator Racc.
-template <int SLOTS, int VEC, class F, bool VJ, class SM, class RA>
+template <int SLOTS, int VEC, class F, bool VJ, class SM, class RA, bool JW = false>
 __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
                              int64_t u, int lane, RA& Racc) {
   constexpr bool FUSED = !std::is_same<F, NoFuse>::value;
@@ -441,7 +452,8 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         sm.hco[rr] = hc;
         sm.wt[rr] = v;
         sm.segfl[rr] = make_int2((int)sg, fl);
-        if ((fl & 2) && a.scales) {
+        sm.hsc[rr] = sc;
+        if ((fl & 2) && a.scales && a.wj < 0) {
           const int64_t hi = a.head_index ? a.head_index[sg] : sg;
           a.scales[hi] = a.scale_count ? sqrt((double)a.scale_count[sg]) : sc;
         }
@@ -533,6 +545,24 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
           hc = sm.hco[rr];
         }
         const double* row = sm.buf + rr * geo.ls;
+        // Join-on-write factors of this group (process_and_join_children,
+        // figaro.hpp:196-230, in its product order).
+        double jsc[kVJMax];
+        int jidx[kVJMax];
+        double jall = 1.0;
+        const bool jwrite = JW && !FUSED && hrow && a.wj >= 0;
+        if (jwrite) {
+#pragma unroll
+          for (int c = 0; c < kVJMax; ++c) {
+            jsc[c] = 0.0;
+            jidx[c] = -1;
+            if (c < a.wj) {
+              jidx[c] = a.wlidx[c][sf.x];
+              jsc[c] = jidx[c] >= 0 ? a.wsc[c][jidx[c]] : 0.0;
+              jall *= jsc[c];
+            }
+          }
+        }
 #pragma unroll
         for (int s = 0; s < SLOTS; ++s) {
           const int pk = cl + geo.L * s;
@@ -570,8 +600,32 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
               trow[pk] = o[0];
           }
           if (hrow) {
+            if (jwrite) {
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) hrow[VEC * pk + e] = run[s][e] * hc;
+              for (int e = 0; e < VEC; ++e) hrow[VEC * pk + e] = (run[s][e] * hc) * jall;
+            } else {
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) hrow[VEC * pk + e] = run[s][e] * hc;
+            }
+          }
+        }
+        if (jwrite) {
+          // The children's summary columns of the joined row, and its scale.
+          const double sk = sm.hsc[rr];
+          for (int col = w + cl; col < a.wwidth; col += geo.L) {
+            int c = 0;
+            while (c + 1 < a.wj && col >= a.woff[c + 1]) ++c;
+            double f = sk;
+#pragma unroll
+            for (int d = 0; d < kVJMax; ++d)
+              if (d != c && d < a.wj) f *= jsc[d];
+            hrow[col] = jidx[c] >= 0
+                            ? a.wS[c][(int64_t)jidx[c] * a.wcw[c] + (col - a.woff[c])] * f
+                            : 0.0;
+          }
+          if (cl == 0 && a.scales) {
+            const int64_t hi = a.head_index ? a.head_index[sf.x] : sf.x;
+            a.scales[hi] = sk * jall;
           }
         }
       }
@@ -601,7 +655,7 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
   }
 }
 
-template <int SLOTS, int VEC, bool VJ>
+template <int SLOTS, int VEC, bool VJ, bool JW = false>
 __global__ void __launch_bounds__(kWarps * 32)
     k_heads_tails(HtDev a, Geo geo) {
   using SMT = std::conditional_t<VJ, WarpSmemVJ, WarpSmem>;
@@ -616,7 +670,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     if (lane == 0) u = atomicAdd(a.ticket, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= a.n_units) break;
-    process_unit<SLOTS, VEC, NoFuse, VJ>(a, geo, sm, u, lane, dummy);
+    process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW>(a, geo, sm, u, lane, dummy);
   }
 }
 
@@ -945,10 +999,10 @@ __global__ void __launch_bounds__(256) k_join_elems2(const __grid_constant__ Joi
   }
 }
 
-template <int SLOTS, int VEC, bool VJ>
+template <int SLOTS, int VEC, bool VJ, bool JW = false>
 void launch_main(Context& ctx, const HtDev& d, const Geo& geo) {
   const size_t smem = (VJ ? sizeof(WarpSmemVJ) : sizeof(WarpSmem)) * kWarps;
-  auto kern = k_heads_tails<SLOTS, VEC, VJ>;
+  auto kern = k_heads_tails<SLOTS, VEC, VJ, JW>;
   FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   int per_sm = 0;
@@ -971,6 +1025,12 @@ void launch_slots(Context& ctx, const HtDev& d, const Geo& geo) {
     if (slots <= 1) launch_main<1, VEC, true>(ctx, d, geo);
     else if (slots <= 2) launch_main<2, VEC, true>(ctx, d, geo);
     else launch_main<4, VEC, true>(ctx, d, geo);
+    return;
+  }
+  if (d.wj >= 0) {  // join-on-write: own widths up to 2 packets per lane
+    if (slots > 2) fail(FG_E_UNSUPPORTED, "join-on-write: own width too large");
+    if (slots <= 1) launch_main<1, VEC, false, true>(ctx, d, geo);
+    else launch_main<2, VEC, false, true>(ctx, d, geo);
     return;
   }
   if (slots <= 1) launch_main<1, VEC, false>(ctx, d, geo);
@@ -1023,6 +1083,21 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   d.ldt = in.ldt;
   d.scales = in.scales;
   d.nj = -1;
+  d.wj = -1;
+  if (in.join_write) {
+    const JoinArgs& j = *in.join_write;
+    if (j.n_children > kVJMax) fail(FG_E_ARG, "join-on-write: too many children");
+    if (j.own_w != in.w || in.ldh < j.width) fail(FG_E_ARG, "join-on-write: layout");
+    d.wj = j.n_children;
+    d.wwidth = (int)j.width;
+    for (int c = 0; c < j.n_children; ++c) {
+      d.wlidx[c] = j.lidx[c];
+      d.wS[c] = j.child_S[c];
+      d.wsc[c] = j.child_scale[c];
+      d.wcw[c] = j.child_w[c];
+      d.woff[c] = j.child_off[c];
+    }
+  }
   if (in.join) {
     const JoinArgs& j = *in.join;
     if (j.n_children > kVJMax) fail(FG_E_ARG, "join-on-read: too many children");
@@ -1115,6 +1190,14 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   geo.L = 1;
   while (geo.L < geo.np && geo.L < 32) geo.L <<= 1;
   geo.G = 32 / geo.L;
+  // Row-groups of exactly np lanes when that packs more rows into the warp
+  // (C3's project-away, 10 packets: 3 row-groups / 30 busy lanes instead of
+  // 2 / 20); the lanes past G * L idle.  Unfused kernels only.
+  if (rb_fixed == 0 && in.w > 0 && !in.join && geo.np < 32 && 32 / geo.np > geo.G &&
+      getenv("FG_HT_POW2") == nullptr) {
+    geo.L = geo.np;
+    geo.G = 32 / geo.np;
+  }
   if (in.w > 0) {
     int rb = std::min(in.join ? kVJRows : kMaxRB, kSmemDoubles / in.w);
     if (rb >= geo.G) rb -= rb % geo.G;

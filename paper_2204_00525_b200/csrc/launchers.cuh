@@ -116,10 +116,12 @@ struct ChildLinks {
   int n;
   const int* lidx[kMaxChildren];       // own segment -> child parent-key idx
   uint64_t* phi_down[kMaxChildren];
-  uint64_t* phi_up[kMaxChildren];
+  uint64_t* phi_up[kMaxChildren];  // 2 P entries each (split accumulation)
+  int64_t P[kMaxChildren];
 };
+// phi_down (own parent-key table) has 2 P entries, zeroed by the caller.
 void launch_theta(Context& ctx, const uint64_t* sizes, int64_t G,
-                  const ChildLinks& ch, const int* pidx, uint64_t* phi_down,
+                  const ChildLinks& ch, const int* pidx, uint64_t* phi_down, int64_t P,
                   uint64_t* theta, unsigned* status);
 void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
                 int64_t G, const int* pidx, const uint64_t* phi_up,
@@ -154,6 +156,12 @@ struct HeadTailArgs {
   const JoinArgs* join = nullptr;
   const double* join_heads = nullptr;
   int64_t join_ldh = 0;
+  // Join-on-write (K4 folded into K3's head emission): the head row of group
+  // g is written as the joined summary row -- own columns times prod_c s_c,
+  // child columns from the children's summaries -- and `scales` receives the
+  // joined scale sqrt(m_g) * prod_c s_c.  Uses join->n_children, lidx,
+  // child_S, child_scale, child_w, child_off; `heads`/`ldh` is the summary.
+  const JoinArgs* join_write = nullptr;
 };
 // Runs the segmented (generalized) head/tail transform.  Needs the max
 // segment size only to decide whether the heavy-segment pre-pass runs.

@@ -551,8 +551,9 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     n.theta.alloc(n.grp.G, st);
     n.fjs.alloc(n.grp.G, st);
     n.circ.alloc(n.grp.G, st);
-    n.phi_down.alloc(n.P, st);
-    n.phi_up.alloc(n.P, st);
+    // 2 P: low/high-word accumulators of the split sums (counts.cu add_split)
+    n.phi_down.alloc(2 * n.P, st);
+    n.phi_up.alloc(2 * n.P, st);
     n.phi_down.zero();
     n.phi_up.zero();
   }
@@ -565,13 +566,14 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       ch.lidx[k] = n.lidx[k].get();
       ch.phi_down[k] = c.phi_down.get();
       ch.phi_up[k] = c.phi_up.get();
+      ch.P[k] = c.P;
     }
     return ch;
   };
   for (auto it = preorder.rbegin(); it != preorder.rend(); ++it) {
     NodeState& n = *nodes[*it];
     launch_theta(ctx, n.sizes.get(), n.grp.G, links(n),
-                 n.parent >= 0 ? n.pidx.get() : nullptr, n.phi_down.get(),
+                 n.parent >= 0 ? n.pidx.get() : nullptr, n.phi_down.get(), n.P,
                  n.theta.get(), ctx.status.get());
   }
   for (int i : preorder) {
@@ -619,6 +621,29 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     const bool fuse = opt.fuse && !opt.keep_r0 && fused_width(n.w) > 0 && n_tails > 0 &&
                       n_tails * 10 >= n.rows * 7;
     if (n.w > 0 && n_tails > 0 && !fuse) n.tails.alloc(n_tails * n.w, st);
+    JoinArgs j{};
+    if (!is_leaf) {
+      j.G = G;
+      j.own_w = n.w;
+      j.S = n.S.get();
+      j.width = n.width;
+      j.scale = n.scale.get();
+      j.n_children = (int)n.children.size();
+      for (int k = 0; k < j.n_children; ++k) {
+        NodeState& c = *nodes[n.children[k]];
+        j.lidx[k] = n.lidx[k].get();
+        j.child_S[k] = c.sum_S;
+        j.child_scale[k] = c.sum_scale;
+        j.child_w[k] = (int)c.width;
+        j.child_off[k] = (int)(lay.sub_begin[n.children[k]] - lay.sub_begin[i]);
+      }
+    }
+    // Join-on-write: the unfused own heads/tails kernel emits the joined
+    // summary rows and scales itself (no separate K4 pass over S).  Measured
+    // slower on C3 (figaro 18.9 -> 20.5 ms: the child lookups stall the
+    // head emission), so it is opt-in (FG_JOIN_ON_WRITE=1).
+    const bool jw = !is_leaf && !vj && !fuse && n.w > 0 && n.w <= 16 && G > 0 &&
+                    (int)n.children.size() <= 4 && getenv("FG_JOIN_ON_WRITE") != nullptr;
     if (host_in) FG_CUDA(cudaStreamWaitEvent(st, up.data[i], 0));
     HeadTailArgs a;
     a.data = n.data;
@@ -635,6 +660,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     a.tails = n.tails.get();
     a.ldt = n.w;
     a.scales = n.scale.get();
+    a.join_write = jw ? &j : nullptr;
     kt_ht.begin();
     if (fuse) {
       n.fused_count = run_heads_tails_fused(ctx, a, n.fused);
@@ -649,34 +675,19 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     kt_ht.end();
     // input elements read once + heads written once (+ tails written once
     // when they go to HBM; fused tails stay on chip)
+    // (+ the children's summary columns of the joined rows with join-on-write)
     ht_bytes += 8.0 * ((double)n.rows * n.w + (double)G * n.w +
-                       (n.fused_count ? 0.0 : (double)n_tails * n.w));
+                       (n.fused_count ? 0.0 : (double)n_tails * n.w) +
+                       (jw ? (double)G * (n.width - n.w) : 0.0));
     if (n.fused_count) {
       ++fused_launches;
       fused_flops += span_flops((double)n_tails, n.w);
     }
-    JoinArgs j{};
-    if (!is_leaf) {
-      j.G = G;
-      j.own_w = n.w;
-      j.S = n.S.get();
-      j.width = n.width;
-      j.scale = n.scale.get();
+    if (!is_leaf && !vj && !jw) {
       n.scale_j.alloc(G, st);
       j.scale_out = n.scale_j.get();
-      j.n_children = (int)n.children.size();
-      for (int k = 0; k < j.n_children; ++k) {
-        NodeState& c = *nodes[n.children[k]];
-        j.lidx[k] = n.lidx[k].get();
-        j.child_S[k] = c.sum_S;
-        j.child_scale[k] = c.sum_scale;
-        j.child_w[k] = (int)c.width;
-        j.child_off[k] = (int)(lay.sub_begin[n.children[k]] - lay.sub_begin[i]);
-      }
-      if (!vj) {
-        launch_join(ctx, j);
-        std::swap(n.scale, n.scale_j);  // joined scales replace the head scales
-      }
+      launch_join(ctx, j);
+      std::swap(n.scale, n.scale_j);  // joined scales replace the head scales
     }
     if (!is_root && !is_leaf) {
       n.Sq.alloc(n.P * n.width, st);
@@ -1052,8 +1063,11 @@ fg_status fg_get_counts(fg_ctx* c, int32_t node, int32_t kind, uint64_t* out) {
       default: fail(FG_E_ARG, "unknown count kind");
     }
     if (kind >= FG_PHI_DOWN && n.parent < 0) return;
-    if (src->size())
-      FG_CUDA(cudaMemcpy(out, src->get(), src->bytes(), cudaMemcpyDeviceToHost));
+    // phi tables carry 2 P entries (split accumulation, counts.cu): the
+    // first P are the final values.
+    const int64_t cnt = kind >= FG_PHI_DOWN ? n.P : n.grp.G;
+    if (cnt > (int64_t)src->size()) fail(FG_E_ARG, "count table shorter than its keys");
+    if (cnt) FG_CUDA(cudaMemcpy(out, src->get(), cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   });
 }
 

@@ -693,6 +693,9 @@ void radix_sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out, const i
     const char* e = getenv("FG_SORT_LB");
     return e && std::string(e) == "1" ? 1 : 4;
   }();
+  // (A persistent two-buffer variant that prefetched its next ticket was
+  // measured 10x slower: tiles prefetched but not yet ranked stall every
+  // later tile's look-back.)
   auto kern = lb == 1 ? k_onesweep<KeyT, 1> : k_onesweep<KeyT, 4>;
   FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
