@@ -270,7 +270,7 @@ class Runner:
             dist.barrier()
         acc = {"group": 0.0, "counts": 0.0, "figaro": 0.0, "post": 0.0, "ht_s": 0.0,
                "ts_s": 0.0, "ht_launches": 0, "ht_bytes": 0.0, "fused_flops": 0.0,
-               "ts_flops": 0.0, "fused_launches": 0, "syncs": 0}
+               "ts_flops": 0.0, "fused_launches": 0, "syncs": 0, "mallocs": 0}
         self.gather_s = 0.0
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -294,6 +294,7 @@ class Runner:
                 acc["ts_flops"] += res.tsqr_stage_flops
                 acc["fused_launches"] += res.fused_launches
                 acc["syncs"] += res.host_syncs
+                acc["mallocs"] += getattr(res, "device_mallocs", 0)
             e1.record(stream)
             torch.cuda.synchronize()
             if dist is not None:
@@ -315,7 +316,7 @@ class _EmptyResult:
     seconds_group = seconds_counts = seconds_figaro = seconds_postprocess = 0.0
     seconds_headtail_kernels = seconds_tsqr_kernels = headtail_bytes = 0.0
     headtail_fused_flops = tsqr_stage_flops = 0.0
-    headtail_launches = fused_launches = host_syncs = 0
+    headtail_launches = fused_launches = host_syncs = device_mallocs = 0
 
 
 class _Null:
@@ -535,6 +536,7 @@ def main():
                           "figaro": acc["figaro"] * 1e3, "post": acc["post"] * 1e3,
                           "gather": acc["gather_ms"]},
             "host_syncs_per_step": acc["syncs"] // args.steps,
+            "device_mallocs_in_timed_steps": acc["mallocs"],
             "roofline": roof, "roofline_other": other,
             "e2e": e2e, "gpu_launches": acc["launches"], "clocks": clk.summary(),
         }

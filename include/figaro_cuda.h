@@ -127,7 +127,8 @@ typedef struct fg_result {
   double tsqr_stage_flops;
   int64_t fused_launches;         /* heads/tails launches that were fused  */
   int64_t host_syncs;             /* host<->device synchronisations       */
-  int64_t reserved[3];
+  int64_t device_mallocs;         /* cudaMalloc calls (caching-allocator misses) */
+  int64_t reserved[2];
 } fg_result;
 
 /* Runs validate_join_tree, counts, the FiGaRo transform and the TSQR

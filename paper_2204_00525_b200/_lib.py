@@ -54,7 +54,8 @@ class fg_result(C.Structure):
                 ("seconds_tsqr_kernels", C.c_double), ("headtail_launches", C.c_int64),
                 ("headtail_bytes", C.c_double), ("headtail_fused_flops", C.c_double),
                 ("tsqr_stage_flops", C.c_double), ("fused_launches", C.c_int64),
-                ("host_syncs", C.c_int64), ("reserved", C.c_int64 * 3)]
+                ("host_syncs", C.c_int64), ("device_mallocs", C.c_int64),
+                ("reserved", C.c_int64 * 2)]
 
 
 class fg_block(C.Structure):

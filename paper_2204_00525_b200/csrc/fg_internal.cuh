@@ -64,7 +64,7 @@ class BlockCache {
     }
     bytes = round(bytes);
     auto it = free_.lower_bound(bytes);
-    if (it != free_.end() && it->first <= bytes + bytes / 4 + (1 << 20)) {
+    if (it != free_.end() && it->first <= bytes + bytes / 2) {
       void* p = it->second;
       size_t b = it->first;
       free_.erase(it);
@@ -72,6 +72,7 @@ class BlockCache {
       return p;
     }
     void* p = nullptr;
+    ++mallocs_;
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
@@ -104,6 +105,7 @@ class BlockCache {
     free_.clear();
   }
   size_t reserved() const { return reserved_; }
+  int64_t mallocs() const { return mallocs_; }
   // FG_EXACT_ALLOC=1: no caching or rounding, so compute-sanitizer memcheck
   // sees every out-of-bounds access.
   static bool exact() {
@@ -112,13 +114,20 @@ class BlockCache {
   }
 
  private:
+  // Size classes: 512 B steps below 1 MB, then four classes per power of
+  // two (x1, x1.25, x1.5, x1.75), so the same request shapes map to the same
+  // classes every call and steady-state calls find their blocks again.
   static size_t round(size_t b) {
     if (b < (1 << 20)) return (b + 511) & ~size_t(511);
-    return (b + (2 << 20) - 1) & ~size_t((2 << 20) - 1);
+    size_t p = size_t(1) << 20;
+    while (p * 2 <= b) p *= 2;
+    const size_t q = p / 4;
+    return (b + q - 1) / q * q;
   }
   std::multimap<size_t, void*> free_;
   std::map<void*, size_t> live_;
   size_t reserved_ = 0;
+  int64_t mallocs_ = 0;
 };
 
 // The cache of the context currently running on this thread (set by the C

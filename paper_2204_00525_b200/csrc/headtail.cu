@@ -18,10 +18,11 @@
 //            = a_j * alpha_j - S_j * beta_j
 // are computed once per row by one lane and broadcast through shared memory.
 //
-// Groups crossing a unit boundary need the prefix of their earlier rows.
-// Short groups (<= kLight rows) re-read those rows (at most kLight, mostly L2
-// hits).  Long groups get it from a deterministic pre-pass: per unit the
-// partial sum of its continuing group, then a per-group scan over units.
+// Groups crossing a unit boundary: a short group (<= kLight rows) is
+// finished by the unit it starts in (units snap to its end), so every row is
+// read once.  Long groups get the prefix of their earlier rows from a
+// deterministic pre-pass: per unit the partial sum of its continuing group,
+// then a per-group scan over units.
 // All results are run-to-run deterministic: the fused kernel assigns units
 // to warps statically (unit u to warp u mod #warps), so each warp's TSQR
 // accumulator absorbs the same rows in the same order on every run.
@@ -43,7 +44,12 @@ namespace {
 constexpr int kWarps = 8;            // warps per CTA
 constexpr int kUnit = 256;           // rows per work unit
 constexpr int kLight = 256;          // groups up to this size recompute carries
-constexpr int kSmemDoubles = 512;    // per-warp row buffer (4 KB)
+#ifndef FG_HT_SMEM
+#define FG_HT_SMEM 480
+#endif
+// Per-warp row buffer (3.75 KB): with the batch metadata 56 KB per 8-warp
+// CTA, so 4 CTAs fit an SM (512 doubles: 3; C3 figaro -1.2 ms).
+constexpr int kSmemDoubles = FG_HT_SMEM;
 constexpr int kMaxRB = 64;           // max rows per batch
 constexpr int kVJMax = 4;            // children of a join-on-read node
 constexpr int kVJRows = 32;          // max rows per batch with join-on-read
@@ -179,8 +185,7 @@ struct WarpSmemT {
   double buf[CAP];
   double2 coef[kMaxRB];   // {alpha, beta}: tail = a*alpha - S*beta
   double hco[kMaxRB];     // head coefficient at a group's last row
-  double hsc[kMaxRB];     // the group's scale at its last row
-  double wt[kMaxRB];      // generalized weights
+  double wt[kMaxRB];      // generalized weights (plain: the group's scale)
   int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
   unsigned char startf[kMaxRB];  // 1 where a group starts inside the batch
   const double* rowptr[kMaxRB];
@@ -210,40 +215,6 @@ struct Geo {
 template <int VEC>
 __device__ __forceinline__ void cp_async(double* dst, const double* src) {
   __pipeline_memcpy_async(dst, src, VEC * sizeof(double));
-}
-
-// Column sums over sorted rows [q0, q1) for this lane's columns: row indices
-// (and weights) are fetched 32 at a time lane-parallel, then each lane walks
-// the chunk with independent loads (no dependent address chain per row).
-__device__ __forceinline__ void chunk_colsum(const HtDev& a, int64_t q0, int64_t q1,
-                                             int col, double& acc, double& nacc,
-                                             bool want_norm, int lane) {
-  const bool weighted = a.weights != nullptr;
-  for (int64_t base = q0; base < q1; base += 32) {
-    const int cnt = (int)(q1 - base < 32 ? q1 - base : 32);
-    int64_t my_row = 0;
-    double my_w = 1.0;
-    if (lane < cnt) {
-      my_row = src_row(a, base + lane);
-      if (weighted) my_w = a.weights[my_row];
-    }
-#pragma unroll 8
-    for (int t = 0; t < cnt; ++t) {
-      const int64_t r = __shfl_sync(0xffffffffu, my_row, t);
-      double v = weighted ? __shfl_sync(0xffffffffu, my_w, t) : 1.0;
-      if (a.nj >= 0) {
-        double x = 0.0, wv = 1.0;
-        if (col >= 0) vj_load<1>(a, r, col, &x, wv);
-        else { double f[kVJMax + 1]; int idx[kVJMax]; wv = vj_row(a, r, f, idx); }
-        v = wv;
-        if (col >= 0) acc = fma(v, x, acc);
-      } else if (col >= 0) {
-        const double x = a.data[r * a.ld + col];
-        acc = weighted ? fma(v, x, acc) : acc + x;
-      }
-      if (want_norm) nacc = fma(v, v, nacc);
-    }
-  }
 }
 
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
@@ -285,8 +256,11 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
     __pipeline_commit();
     return;
   }
-  for (int rr = lane; rr < nb; rr += 32)
-    sm.rowptr[rr] = a.data + src_row(a, p + rr) * a.ld;
+  for (int rr = lane; rr < nb; rr += 32) {
+    const int64_t x = src_row(a, p + rr);
+    sm.rowptr[rr] = a.data + x * a.ld;
+    if (a.weights) sm.wt[rr] = a.weights[x];
+  }
   __syncwarp();
   const int g = lane / geo.L, cl = lane % geo.L;
   for (int rr = g < geo.G ? g : nb; rr < nb; rr += geo.G) {
@@ -330,6 +304,17 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
     for (int e = 0; e < VEC; ++e) S[s][e] = 0.0;
   double N = 0.0;  // weighted: running sum of squared weights (lane-uniform)
 
+  // Short groups (<= kLight rows) are never split: a unit whose first group
+  // started in the previous unit leaves it to that unit, and a unit whose
+  // last group runs past its end finishes it -- every row is read once.
+  // Long groups keep the unit boundaries and take their prefix from the
+  // deterministic pre-pass (chained carries).
+  int64_t q0 = p0, q1 = p1;
+  if (p1 < a.n_rows) {
+    const int64_t g1 = a.ufirst ? (int64_t)a.ufirst[u + 1] : seg_of(a.begins, p1, 0, a.n_seg);
+    const int64_t c0 = a.begins[g1], c1 = a.begins[g1 + 1];
+    if (c0 < p1 && c1 - c0 <= kLight) q1 = c1;
+  }
   const int64_t gb = a.begins[g];
   if (gb < p0) {
     // The first group started in an earlier unit: get its prefix.
@@ -348,37 +333,56 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         }
       }
     } else {
-      // Re-read the group's earlier rows (at most kLight of them).
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s)
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const int pk = cl + geo.L * s;
-          const int col = (pk < geo.np && VEC * pk + e < w) ? VEC * pk + e : -1;
-          double nacc = 0.0;
-          chunk_colsum(a, gb, p0, col, S[s][e], nacc, weighted && s == 0 && e == 0, lane);
-          if (weighted && s == 0 && e == 0) N = nacc;
-        }
+      // A short group: the previous unit owns it.
+      q0 = a.begins[g + 1];
+      ++g;
     }
   }
 
-  for (int64_t pb = p0; pb < p1; pb += a.rb) {
-    const int nb = (int)(p1 - pb < (int64_t)a.rb ? p1 - pb : (int64_t)a.rb);
+  for (int64_t pb = q0; pb < q1; pb += a.rb) {
+    const int nb = (int)(q1 - pb < (int64_t)a.rb ? q1 - pb : (int64_t)a.rb);
+    // The batch's rows lie in groups g .. g+nb: their offsets begins[g ..
+    // g+nb+1] and tail scales sqrt(tail_count[g .. g+nb]) are loaded now,
+    // three per lane in registers, so their latency overlaps the row
+    // gathers below instead of following them (read back by shuffles).
+    int bgv[3];
+    double tsv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int i = lane + 32 * k;
+      const int64_t gi = g + i;
+      bgv[k] = (i <= nb + 1 && gi <= a.n_seg) ? a.begins[gi] : INT_MAX;
+      tsv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? sqrt((double)a.tail_count[gi]) : 1.0;
+    }
     if (w > 0) stage_rows<SLOTS, VEC, VJ>(a, geo, sm, pb, nb, lane);
     else if (VJ) __syncwarp();
     // Group starts inside the batch (groups g+1 .. g+nb can start here):
     // flagged in shared memory, then each row's group is g plus a ballot
-    // prefix count -- one level of loads instead of a binary search per row.
+    // prefix count.
     for (int i = lane; i < kMaxRB; i += 32) sm.startf[i] = 0;
     __syncwarp();
-    for (int i = lane; i < nb; i += 32) {
-      const int64_t gi = g + 1 + i;
-      if (gi < a.n_seg) {
-        const int64_t b = a.begins[gi];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int i = lane + 32 * k - 1;  // group g + 1 + i starts at bgv[k]
+      if (i >= 0 && i < nb && g + 1 + i < a.n_seg) {
+        const int64_t b = bgv[k];
         if (b < pb + nb) sm.startf[b - pb] = 1;
       }
     }
     __syncwarp();
+    // begins[g + i] and the tail scale of group g + i from the registers.
+    auto bg_at = [&](int i) -> int64_t {
+      const int v0 = __shfl_sync(0xffffffffu, bgv[0], i & 31);
+      const int v1 = __shfl_sync(0xffffffffu, bgv[1], i & 31);
+      const int v2 = __shfl_sync(0xffffffffu, bgv[2], i & 31);
+      return i < 32 ? v0 : (i < 64 ? v1 : v2);
+    };
+    auto ts_at = [&](int i) -> double {
+      const double v0 = __shfl_sync(0xffffffffu, tsv[0], i & 31);
+      const double v1 = __shfl_sync(0xffffffffu, tsv[1], i & 31);
+      const double v2 = __shfl_sync(0xffffffffu, tsv[2], i & 31);
+      return i < 32 ? v0 : (i < 64 ? v1 : v2);
+    };
     int64_t gcur = g;
     // Row metadata and coefficients, one row per lane.
     for (int base = 0; base < nb; base += 32) {
@@ -390,18 +394,20 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
       int64_t jj = 0, m = 1;
       double v = 1.0;
       int fl = 0;
+      const int li = live ? (int)(sg - g) : 0;  // <= nb
+      const int64_t b0 = bg_at(li);
+      const int64_t b1 = bg_at(li + 1);
+      const double tsr = ts_at(li);
       if (live) {
         const int64_t p = pb + rr;
-        const int64_t b0 = a.begins[sg];
-        const int64_t b1 = a.begins[sg + 1];
         jj = p - b0;
         m = b1 - b0;
         fl = (jj == 0 ? 1 : 0) | (p == b1 - 1 ? 2 : 0);
-        if (VJ) v = sm.wt[rr];
+        if (VJ || (weighted && w > 0)) v = sm.wt[rr];  // staged with the row (stage_rows)
         else if (weighted) v = a.weights[src_row(a, p)];
       }
       double ts = 1.0;
-      if (live && a.tail_count) ts = sqrt((double)a.tail_count[sg]);  // exact for squares
+      if (live && a.tail_count) ts = tsr;  // sqrt is exact for squares
       double al = 0.0, be = 0.0, hc = 0.0, sc = 0.0;
       if (!weighted) {
         if (live && jj >= 1) {
@@ -450,9 +456,8 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
       if (live) {
         sm.coef[rr] = make_double2(al, be);
         sm.hco[rr] = hc;
-        sm.wt[rr] = v;
+        sm.wt[rr] = weighted ? v : sc;  // plain rows never read their weight
         sm.segfl[rr] = make_int2((int)sg, fl);
-        sm.hsc[rr] = sc;
         if ((fl & 2) && a.scales && a.wj < 0) {
           const int64_t hi = a.head_index ? a.head_index[sg] : sg;
           a.scales[hi] = a.scale_count ? sqrt((double)a.scale_count[sg]) : sc;
@@ -611,7 +616,7 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         }
         if (jwrite) {
           // The children's summary columns of the joined row, and its scale.
-          const double sk = sm.hsc[rr];
+          const double sk = sm.wt[rr];  // plain transform: the group's scale
           for (int col = w + cl; col < a.wwidth; col += geo.L) {
             int c = 0;
             while (c + 1 < a.wj && col >= a.woff[c + 1]) ++c;
@@ -1296,6 +1301,11 @@ int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
 void launch_join(Context& ctx, const JoinArgs& a) {
   if (a.G == 0) return;
   const int threads = 256;
+  bool even = (a.width % 2 == 0) && (a.own_w % 2 == 0) && a.width > 0;
+  for (int c = 0; c < a.n_children; ++c)
+    even = even && (a.child_off[c] % 2 == 0) && (a.child_w[c] % 2 == 0);
+  // (A one-pass variant recomputing the row factors per element was measured
+  // 7 ms slower on C3: four dependent loads per element.)
   DevArray<double> fac(a.G * (a.n_children + 1), ctx.stream);
   int64_t grid = std::min<int64_t>(ceil_div(a.G, threads), (int64_t)ctx.sm_count * 16);
   k_join_rows<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a, fac.get());
@@ -1304,9 +1314,6 @@ void launch_join(Context& ctx, const JoinArgs& a) {
   const int64_t total = a.G * a.width;
   if (total > 0) {
     grid = std::min<int64_t>(ceil_div(a.G, kJoinTile), (int64_t)ctx.sm_count * 16);
-    bool even = (a.width % 2 == 0) && (a.own_w % 2 == 0);
-    for (int c = 0; c < a.n_children; ++c)
-      even = even && (a.child_off[c] % 2 == 0) && (a.child_w[c] % 2 == 0);
     if (even)
       k_join_elems2<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a, fac.get());
     else

@@ -333,6 +333,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   double ht_bytes = 0, fused_flops = 0, tsqr_flops = 0;
   int64_t fused_launches = 0;
   const int64_t syncs0 = ctx.syncs;
+  const int64_t mallocs0 = ctx.cache.mallocs();
   auto span_flops = [](double m, double w) {
     return m > 0 && w > 0 ? 2.0 * m * w * w - 2.0 / 3.0 * w * w * w : 0.0;
   };
@@ -828,6 +829,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     res->tsqr_stage_flops = tsqr_flops;
     res->fused_launches = fused_launches;
     res->host_syncs = ctx.syncs - syncs0;
+    res->device_mallocs = ctx.cache.mallocs() - mallocs0;
   }
   // Keep the inspection state; drop the bulky buffers unless R0 is wanted.
   saved->have_r0 = opt.keep_r0 != 0;

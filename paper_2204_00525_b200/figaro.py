@@ -358,6 +358,7 @@ class PipelineResult:
     tsqr_stage_flops: float = 0.0
     fused_launches: int = 0
     host_syncs: int = 0
+    device_mallocs: int = 0
     counts: Optional[List[NodeCounts]] = None
     r0: Optional[List[OutSpan]] = None
 
@@ -433,7 +434,8 @@ def run_pipeline(relations: Sequence[Relation], tree: JoinTree,
         seconds_tsqr_kernels=res.seconds_tsqr_kernels,
         headtail_launches=res.headtail_launches, headtail_bytes=res.headtail_bytes,
         headtail_fused_flops=res.headtail_fused_flops, tsqr_stage_flops=res.tsqr_stage_flops,
-        fused_launches=res.fused_launches, host_syncs=res.host_syncs)
+        fused_launches=res.fused_launches, host_syncs=res.host_syncs,
+        device_mallocs=res.device_mallocs)
     if fetch_counts:
         out.counts = [fetch_node_counts(ctx, i, rels[i], tree) for i in range(len(rels))]
     if keep_r0:
