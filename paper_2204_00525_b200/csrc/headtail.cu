@@ -79,6 +79,8 @@ struct HtDev {
                          // cont[u-1] == first group of u
   int* ticket;
   const int* ufirst;     // per unit: group of its first row (or null)
+  const int64_t* qb;     // per unit: its first row (n_units + 1 entries, or null)
+  const double* head_mul;  // per group: heads *= head_mul[g] (or null)
   // Join-on-read (K4 folded into K5; process_and_join_children,
   // figaro.hpp:196-230): with nj >= 0 the data row x is never materialised;
   // it is [jhead[x, :own_w] * all | jS[c][jlidx[c][x]] * f_c ...] with
@@ -285,7 +287,13 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
   const int w = a.w;
   const bool weighted = a.weights != nullptr;
   const int64_t p0 = u * kUnit;
-  const int64_t p1 = min(p0 + kUnit, a.n_rows);
+  // Short groups (<= kLight rows) are never split: the unit a short group
+  // starts in finishes it (k_unit_cont moves the next unit's first row,
+  // qb[u + 1], to the group's end), so every row is read once.  Long groups
+  // keep the unit boundaries and take their prefix from the deterministic
+  // pre-pass (chained carries).
+  const int64_t q0 = a.qb ? a.qb[u] : p0;
+  const int64_t q1 = a.qb ? a.qb[u + 1] : min(p0 + kUnit, a.n_rows);
   int64_t g = a.ufirst ? (int64_t)a.ufirst[u] : seg_of(a.begins, p0, 0, a.n_seg);
   const int grp = lane / geo.L, cl = lane % geo.L;
   // Join-on-read: the block (child or own) of each owned column packet.
@@ -304,20 +312,9 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
     for (int e = 0; e < VEC; ++e) S[s][e] = 0.0;
   double N = 0.0;  // weighted: running sum of squared weights (lane-uniform)
 
-  // Short groups (<= kLight rows) are never split: a unit whose first group
-  // started in the previous unit leaves it to that unit, and a unit whose
-  // last group runs past its end finishes it -- every row is read once.
-  // Long groups keep the unit boundaries and take their prefix from the
-  // deterministic pre-pass (chained carries).
-  int64_t q0 = p0, q1 = p1;
-  if (p1 < a.n_rows) {
-    const int64_t g1 = a.ufirst ? (int64_t)a.ufirst[u + 1] : seg_of(a.begins, p1, 0, a.n_seg);
-    const int64_t c0 = a.begins[g1], c1 = a.begins[g1 + 1];
-    if (c0 < p1 && c1 - c0 <= kLight) q1 = c1;
-  }
   const int64_t gb = a.begins[g];
-  if (gb < p0) {
-    // The first group started in an earlier unit: get its prefix.
+  if (gb < q0) {
+    // A long group started in an earlier unit: its prefix from the pre-pass.
     const bool chained = u > 0 && a.cont && a.cont[u - 1] == (int)g;
     const int V = w + (weighted ? 1 : 0);
     const double* cr = chained ? a.carry + u * (int64_t)V : nullptr;
@@ -332,10 +329,6 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
           if (pk < geo.np && col < w) S[s][e] = cr[col];
         }
       }
-    } else {
-      // A short group: the previous unit owns it.
-      q0 = a.begins[g + 1];
-      ++g;
     }
   }
 
@@ -346,13 +339,14 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
     // three per lane in registers, so their latency overlaps the row
     // gathers below instead of following them (read back by shuffles).
     int bgv[3];
-    double tsv[3];
+    double tsv[3], hmv[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const int i = lane + 32 * k;
       const int64_t gi = g + i;
       bgv[k] = (i <= nb + 1 && gi <= a.n_seg) ? a.begins[gi] : INT_MAX;
       tsv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? sqrt((double)a.tail_count[gi]) : 1.0;
+      hmv[k] = (a.head_mul && i <= nb && gi < a.n_seg) ? a.head_mul[gi] : 1.0;
     }
     if (w > 0) stage_rows<SLOTS, VEC, VJ>(a, geo, sm, pb, nb, lane);
     else if (VJ) __syncwarp();
@@ -383,6 +377,12 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
       const double v2 = __shfl_sync(0xffffffffu, tsv[2], i & 31);
       return i < 32 ? v0 : (i < 64 ? v1 : v2);
     };
+    auto hm_at = [&](int i) -> double {
+      const double v0 = __shfl_sync(0xffffffffu, hmv[0], i & 31);
+      const double v1 = __shfl_sync(0xffffffffu, hmv[1], i & 31);
+      const double v2 = __shfl_sync(0xffffffffu, hmv[2], i & 31);
+      return i < 32 ? v0 : (i < 64 ? v1 : v2);
+    };
     int64_t gcur = g;
     // Row metadata and coefficients, one row per lane.
     for (int base = 0; base < nb; base += 32) {
@@ -398,6 +398,7 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
       const int64_t b0 = bg_at(li);
       const int64_t b1 = bg_at(li + 1);
       const double tsr = ts_at(li);
+      const double hmr = a.head_mul ? hm_at(li) : 1.0;
       if (live) {
         const int64_t p = pb + rr;
         jj = p - b0;
@@ -455,7 +456,9 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
       }
       if (live) {
         sm.coef[rr] = make_double2(al, be);
-        sm.hco[rr] = hc;
+        // head_mul: the join's own-column factor prod_c s_c folded into the
+        // head coefficient (figaro.hpp:226, `dst[j] *= all`)
+        sm.hco[rr] = hc * hmr;
         sm.wt[rr] = weighted ? v : sc;  // plain rows never read their weight
         sm.segfl[rr] = make_int2((int)sg, fl);
         if ((fl & 2) && a.scales && a.wj < 0) {
@@ -712,20 +715,32 @@ __global__ void __launch_bounds__(kWarps * 32, F::MINB)
 
 // Pre-pass part 1: per unit (one thread each), does its last group continue
 // into the next unit and is it longer than kLight?  Sets *any if so.
+// Also the unit starts: a short group crossing p1 stays with unit u, so
+// unit u + 1 starts at its end (qb[u + 1], with ufirst[u + 1] its group).
 __global__ void k_unit_cont(HtDev a, int* __restrict__ cont, int* __restrict__ ufirst,
-                            int* any) {
+                            int64_t* __restrict__ qb, int* any) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.n_units;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p0 = u * kUnit;
     const int64_t p1 = min(p0 + kUnit, a.n_rows);
     const int64_t g = seg_of(a.begins, p1 - 1, 0, a.n_seg);
     const int64_t b0 = a.begins[g], b1 = a.begins[g + 1];
-    const bool c = (b1 > p1) && (b1 - b0 > kLight);
+    const bool crosses = b1 > p1;
+    const bool c = crosses && (b1 - b0 > kLight);
     cont[u] = c ? (int)g : -1;
     if (c) *any = 1;
-    // First group of the next unit: g again unless a group starts at p1.
-    if (u + 1 < a.n_units) ufirst[u + 1] = (int)(b1 == p1 ? g + 1 : g);
-    if (u == 0) ufirst[0] = 0;
+    if (u + 1 < a.n_units) {
+      // long crossing group: unit u + 1 continues it at p1; otherwise the next
+      // unit starts with group g + 1 at p1 or (short crossing group) at b1.
+      ufirst[u + 1] = (int)(c ? g : g + 1);
+      qb[u + 1] = (crosses && !c) ? b1 : p1;
+    } else {
+      qb[u + 1] = a.n_rows;
+    }
+    if (u == 0) {
+      ufirst[0] = 0;
+      qb[0] = 0;
+    }
   }
 }
 
@@ -952,7 +967,7 @@ __global__ void __launch_bounds__(256) k_join_elems(const __grid_constant__ Join
       const int64_t k = k0 + kk;
       const double* f = fac + k * (nc + 1);
       if (j < a.own_w) {
-        S[le] *= f[nc];
+        if (!a.own_done) S[le] *= f[nc];
         continue;
       }
       int c = 0;
@@ -981,6 +996,7 @@ __global__ void __launch_bounds__(256) k_join_elems2(const __grid_constant__ Joi
       const int64_t k = k0 + kk;
       const double* f = fac + k * (nc + 1);
       if (j < a.own_w) {
+        if (a.own_done) continue;
         const double m = f[nc];
         double2 v = S[le];
         v.x *= m;
@@ -1001,6 +1017,83 @@ __global__ void __launch_bounds__(256) k_join_elems2(const __grid_constant__ Joi
       }
       S[le] = v;
     }
+  }
+}
+
+// K4 in one kernel over tiles of kJoinTile summary rows: thread t first
+// computes row t's child scales, factors and joined scale (the reference's
+// product order, figaro.hpp:213-228) into shared memory, then the tile's
+// double2 elements are written with a fixed (row, packet) split per thread
+// -- no factor array in HBM, no per-element division.
+constexpr int kJoinMaxC = 4;
+__global__ void __launch_bounds__(kJoinTile) k_join_tile(const __grid_constant__ JoinArgs a) {
+  __shared__ double fs[kJoinTile][kJoinMaxC + 1];  // child factors, [nc] = all
+  __shared__ int is[kJoinTile][kJoinMaxC];
+  const int nc = a.n_children;
+  const int hw = (int)(a.width >> 1);
+  const int tr = threadIdx.x / hw, tp = threadIdx.x - (threadIdx.x / hw) * hw;
+  const int rpp = kJoinTile / hw;  // rows per pass (>= 1)
+  const int j = 2 * tp;
+  int c = 0;
+  if (j >= a.own_w)
+    while (c + 1 < nc && j >= a.child_off[c + 1]) ++c;
+  for (int64_t k0 = blockIdx.x * (int64_t)kJoinTile; k0 < a.G;
+       k0 += (int64_t)gridDim.x * kJoinTile) {
+    const int rows = (int)(a.G - k0 < kJoinTile ? a.G - k0 : kJoinTile);
+    if ((int)threadIdx.x < rows) {
+      const int64_t k = k0 + threadIdx.x;
+      double sc[kJoinMaxC];
+      double all = 1.0;
+#pragma unroll
+      for (int d = 0; d < kJoinMaxC; ++d) {
+        sc[d] = 0.0;
+        if (d < nc) {
+          const int idx = a.lidx[d][k];
+          is[threadIdx.x][d] = idx;
+          sc[d] = idx >= 0 ? a.child_scale[d][idx] : 0.0;
+          all *= sc[d];
+        }
+      }
+      const double sk = a.scale[k];
+      if (a.scale_out) a.scale_out[k] = sk * all;
+      fs[threadIdx.x][kJoinMaxC] = all;
+#pragma unroll
+      for (int d = 0; d < kJoinMaxC; ++d) {
+        if (d >= nc) break;
+        double f = sk;
+#pragma unroll
+        for (int e = 0; e < kJoinMaxC; ++e)
+          if (e != d && e < nc) f *= sc[e];
+        fs[threadIdx.x][d] = f;
+      }
+    }
+    __syncthreads();
+    if (tr < rpp) {
+#pragma unroll 4
+      for (int r = tr; r < rows; r += rpp) {
+        double2* dst = reinterpret_cast<double2*>(a.S + (k0 + r) * a.width) + tp;
+        if (j < a.own_w) {
+          if (a.own_done) continue;
+          const double m = fs[r][kJoinMaxC];
+          double2 v = *dst;
+          v.x *= m;
+          v.y *= m;
+          *dst = v;
+        } else {
+          const int idx = is[r][c];
+          double2 v = make_double2(0.0, 0.0);
+          if (idx >= 0) {
+            const double m = fs[r][c];
+            v = *reinterpret_cast<const double2*>(a.child_S[c] + (int64_t)idx * a.child_w[c] +
+                                                  (j - a.child_off[c]));
+            v.x *= m;
+            v.y *= m;
+          }
+          *dst = v;
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1053,6 +1146,7 @@ struct HtPrep {
   HtDev d{};
   Geo geo{};
   DevArray<int> cont, ticket, ufirst;
+  DevArray<int64_t> qb;
   DevArray<double> val, carry;
 };
 
@@ -1087,6 +1181,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   d.tails = in.tails;
   d.ldt = in.ldt;
   d.scales = in.scales;
+  d.head_mul = in.head_mul;
   d.nj = -1;
   d.wj = -1;
   if (in.join_write) {
@@ -1129,6 +1224,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   DevArray<double>& carry = P.carry;
   cont.alloc(d.n_units, ctx.stream);
   P.ufirst.alloc(d.n_units, ctx.stream);
+  P.qb.alloc(d.n_units + 1, ctx.stream);
   P.ticket.alloc(1, ctx.stream);
   P.ticket.zero();
   d.ticket = P.ticket.get();
@@ -1141,7 +1237,8 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     DevArray<int> any(1, ctx.stream);
     any.zero();
     k_unit_cont<<<(int)std::min<int64_t>(ceil_div(d.n_units, threads), (int64_t)ctx.sm_count * 8),
-                  threads, 0, ctx.stream>>>(d, cont.get(), P.ufirst.get(), any.get());
+                  threads, 0, ctx.stream>>>(d, cont.get(), P.ufirst.get(), P.qb.get(),
+                                            any.get());
     FG_LAUNCHED(ctx);
     FG_KERNEL_CHECK();
     const bool vec2 = in.join ? vj_vec2_ok(in)
@@ -1181,6 +1278,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
     d.cont = cont.get();
     d.carry = carry.get();
     d.ufirst = P.ufirst.get();
+    d.qb = P.qb.get();
   }
   // Vector width, lanes per row-group and rows per batch.
   Geo& geo = P.geo;
@@ -1298,6 +1396,29 @@ int run_heads_tails_fused(Context& ctx, const HeadTailArgs& in,
   }
 }
 
+// all[g] = prod_c s_c of summary row g (figaro.hpp:213-215), for the
+// heads/tails kernel to apply to the own columns as it writes them.
+__global__ void k_join_all(const __grid_constant__ JoinArgs a, double* __restrict__ all_out) {
+  const int nc = a.n_children;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.G;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double all = 1.0;
+    for (int c = 0; c < nc; ++c) {
+      const int idx = a.lidx[c][k];
+      all *= idx >= 0 ? a.child_scale[c][idx] : 0.0;
+    }
+    all_out[k] = all;
+  }
+}
+
+void launch_join_all(Context& ctx, const JoinArgs& a, double* all_out) {
+  if (a.G == 0) return;
+  const int64_t grid = std::min<int64_t>(ceil_div(a.G, 256), (int64_t)ctx.sm_count * 16);
+  k_join_all<<<(int)std::max<int64_t>(grid, 1), 256, 0, ctx.stream>>>(a, all_out);
+  FG_LAUNCHED(ctx);
+  FG_KERNEL_CHECK();
+}
+
 void launch_join(Context& ctx, const JoinArgs& a) {
   if (a.G == 0) return;
   const int threads = 256;
@@ -1306,6 +1427,14 @@ void launch_join(Context& ctx, const JoinArgs& a) {
     even = even && (a.child_off[c] % 2 == 0) && (a.child_w[c] % 2 == 0);
   // (A one-pass variant recomputing the row factors per element was measured
   // 7 ms slower on C3: four dependent loads per element.)
+  if (even && a.width / 2 <= kJoinTile && a.n_children <= kJoinMaxC &&
+      getenv("FG_JOIN_TWO_PASS") == nullptr) {
+    const int64_t grid = std::min<int64_t>(ceil_div(a.G, kJoinTile), (int64_t)ctx.sm_count * 8);
+    k_join_tile<<<(int)std::max<int64_t>(grid, 1), kJoinTile, 0, ctx.stream>>>(a);
+    FG_LAUNCHED(ctx);
+    FG_KERNEL_CHECK();
+    return;
+  }
   DevArray<double> fac(a.G * (a.n_children + 1), ctx.stream);
   int64_t grid = std::min<int64_t>(ceil_div(a.G, threads), (int64_t)ctx.sm_count * 16);
   k_join_rows<<<(int)std::max<int64_t>(grid, 1), threads, 0, ctx.stream>>>(a, fac.get());

@@ -162,6 +162,8 @@ struct HeadTailArgs {
   // joined scale sqrt(m_g) * prod_c s_c.  Uses join->n_children, lidx,
   // child_S, child_scale, child_w, child_off; `heads`/`ldh` is the summary.
   const JoinArgs* join_write = nullptr;
+  // Per-group multiplier of the heads (the join's own-column factor), or null.
+  const double* head_mul = nullptr;
 };
 // Runs the segmented (generalized) head/tail transform.  Needs the max
 // segment size only to decide whether the heavy-segment pre-pass runs.
@@ -187,8 +189,13 @@ struct JoinArgs {
   const double* child_scale[kMaxChildren];
   int child_w[kMaxChildren];
   int child_off[kMaxChildren];  // local column offset in S
+  // The own columns already carry prod_c s_c (heads/tails with head_mul):
+  // only the children's columns and the scales are written.
+  bool own_done = false;
 };
 void launch_join(Context& ctx, const JoinArgs& a);
+// all_out[g] = product of the children's scales of summary row g.
+void launch_join_all(Context& ctx, const JoinArgs& a, double* all_out);
 
 // ---- tsqr.cu ----------------------------------------------------------------
 struct Span {

@@ -51,6 +51,7 @@ struct NodeState {
   DevArray<uint64_t> sizes;
   // parent-key grouping of own segments
   DevArray<int> pa_perm, pa_begins, pidx;
+  bool pa_identity = false;  // parent-key order == own-key order (prefix case)
   DevArray<uint64_t> upk;
   int64_t P = 0;
   PackSpec par{};               // own packed -> parent key (pattr order)
@@ -492,6 +493,7 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       // keys: no sort needed (C3's F under D1, C4's R2 under R1, 2-way joins).
       const bool prefix = n.pattr.size() <= n.key_attr.size() &&
                           std::equal(n.pattr.begin(), n.pattr.end(), n.key_attr.begin());
+      n.pa_identity = prefix;
       if (prefix)
         group_begin_presorted(ctx, ppks[ni].get(), G, nullptr, pgs[ni], ppend[ni],
                               n.pidx.get());
@@ -662,6 +664,18 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
     a.ldt = n.w;
     a.scales = n.scale.get();
     a.join_write = jw ? &j : nullptr;
+    // The join's own-column factor prod_c s_c is applied by the heads/tails
+    // kernel as it writes the heads (no read-modify-write pass over S's own
+    // columns); the join then writes only the children's columns.
+    DevArray<double> hmul;
+    const bool own_mul = !is_leaf && !vj && !jw && n.w > 0 && G > 0 &&
+                         getenv("FG_JOIN_OWN_PASS") == nullptr;
+    if (own_mul) {
+      hmul.alloc(G, st);
+      launch_join_all(ctx, j, hmul.get());
+      a.head_mul = hmul.get();
+      j.own_done = true;
+    }
     kt_ht.begin();
     if (fuse) {
       n.fused_count = run_heads_tails_fused(ctx, a, n.fused);
@@ -707,7 +721,8 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
         b.join_heads = n.S.get();
         b.join_ldh = ldS;
       }
-      b.perm = n.pa_perm.get();
+      // identity order (prefix case): rows read in place, no index loads
+      b.perm = n.pa_identity ? nullptr : n.pa_perm.get();
       b.begins = n.pa_begins.get();
       b.n_seg = n.P;
       b.n_rows = G;
