@@ -45,11 +45,14 @@ constexpr int kWarps = 8;            // warps per CTA
 constexpr int kUnit = 256;           // rows per work unit
 constexpr int kLight = 256;          // groups up to this size recompute carries
 #ifndef FG_HT_SMEM
-#define FG_HT_SMEM 480
+#define FG_HT_SMEM 640
 #endif
 // Per-warp row buffer (3.75 KB): with the batch metadata 56 KB per 8-warp
 // CTA, so 4 CTAs fit an SM (512 doubles: 3; C3 figaro -1.2 ms).
 constexpr int kSmemDoubles = FG_HT_SMEM;
+#ifndef FG_HT_MINB
+#define FG_HT_MINB 3
+#endif
 constexpr int kMaxRB = 64;           // max rows per batch
 constexpr int kVJMax = 4;            // children of a join-on-read node
 constexpr int kVJRows = 32;          // max rows per batch with join-on-read
@@ -190,7 +193,8 @@ struct WarpSmemT {
   double wt[kMaxRB];      // generalized weights (plain: the group's scale)
   int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
   unsigned char startf[kMaxRB];  // 1 where a group starts inside the batch
-  const double* rowptr[kMaxRB];
+  const double* rowptr[kMaxRB];  // staging: source row; afterwards: the row's tail slot (or null)
+  double* hrowp[kMaxRB];         // head row of a group's last row (or null)
   double vjf[VJR][kVJMax + 1];   // join-on-read factors per staged row
   int vjidx[VJR][kVJMax];        // join-on-read child rows per staged row
 };
@@ -207,6 +211,15 @@ __device__ __forceinline__ double fast_rsqrt_d(double q) {
   return r;
 }
 
+// sqrt(q) for q >= 0 finite: q * rsqrt(q) plus one correction step (exact
+// for perfect squares up to 2^52, <= 1 ulp otherwise); 0 for q = 0.
+__device__ __forceinline__ double fast_sqrt_d(double q) {
+  if (!(q > 1e-250 && q < 1e250)) return sqrt(q);
+  const double r = fast_rsqrt_d(q);
+  const double s0 = q * r;
+  return fma(0.5 * r, fma(-s0, s0, q), s0);
+}
+
 // Lane geometry: the warp is split into G row-groups of L lanes; lane cl of
 // a group owns column packets cl + L*s (s < SLOTS) of VEC doubles each.
 // ls: row stride of the staged batch in shared memory (doubles).
@@ -214,14 +227,25 @@ struct Geo {
   int vec, np, L, G, ls;
 };
 
+// Compile-time geometry of the hot unfused shapes (width CW, double2
+// packets, row-groups of exactly CW/2 lanes): the index arithmetic of the
+// batch loops folds into constants.  kW = 0 marks the run-time Geo.
+template <int CW>
+struct GeoC {
+  static constexpr int kW = CW;
+  static constexpr int vec = 2, np = CW / 2, L = CW / 2, G = 32 / (CW / 2), ls = CW;
+};
+template <class GEO> struct GeoW { static constexpr int value = GEO::kW; };
+template <> struct GeoW<Geo> { static constexpr int value = 0; };
+
 template <int VEC>
 __device__ __forceinline__ void cp_async(double* dst, const double* src) {
   __pipeline_memcpy_async(dst, src, VEC * sizeof(double));
 }
 
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
-template <int SLOTS, int VEC, bool VJ, class SM>
-__device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
+template <int SLOTS, int VEC, bool VJ, class SM, class GEO>
+__device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
                                            SM& sm, int64_t p, int nb,
                                            int lane) {
   if constexpr (VJ) {
@@ -280,11 +304,13 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const Geo& geo,
 // F = NoFuse: tails are written to a.tails.  F = WCfg<...>: each batch of
 // tails is written in place into the staged rows (group starts become zero
 // rows) and absorbed into the warp's TSQR accumulator Racc.
-template <int SLOTS, int VEC, class F, bool VJ, class SM, class RA, bool JW = false>
-__device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
+template <int SLOTS, int VEC, class F, bool VJ, class SM, class RA, bool JW = false,
+          class GEO = Geo>
+__device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
                              int64_t u, int lane, RA& Racc) {
   constexpr bool FUSED = !std::is_same<F, NoFuse>::value;
-  const int w = a.w;
+  constexpr int CW = GeoW<GEO>::value;
+  const int w = CW ? CW : a.w;
   const bool weighted = a.weights != nullptr;
   const int64_t p0 = u * kUnit;
   // Short groups (<= kLight rows) are never split: the unit a short group
@@ -332,20 +358,28 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
     }
   }
 
-  for (int64_t pb = q0; pb < q1; pb += a.rb) {
-    const int nb = (int)(q1 - pb < (int64_t)a.rb ? q1 - pb : (int64_t)a.rb);
+  // Rows per batch: a compile-time constant for the specialised shapes (the
+  // host computes the same value, prepare()); KS = 32-entry slices of the
+  // per-group registers (begins / tail scales / head factors) a batch needs.
+  constexpr int kRbC = CW ? ((kMaxRB < kSmemDoubles / (CW ? CW : 1) ? kMaxRB : kSmemDoubles / (CW ? CW : 1)) /
+                             (CW ? 32 / (CW / 2) : 1)) * (CW ? 32 / (CW / 2) : 1)
+                          : 0;
+  constexpr int KS = (CW && !FUSED) ? (kRbC + 1) / 32 + 1 : 3;
+  const int rbv = (CW && !FUSED) ? kRbC : a.rb;
+  for (int64_t pb = q0; pb < q1; pb += rbv) {
+    const int nb = (int)(q1 - pb < (int64_t)rbv ? q1 - pb : (int64_t)rbv);
     // The batch's rows lie in groups g .. g+nb: their offsets begins[g ..
     // g+nb+1] and tail scales sqrt(tail_count[g .. g+nb]) are loaded now,
     // three per lane in registers, so their latency overlaps the row
     // gathers below instead of following them (read back by shuffles).
-    int bgv[3];
-    double tsv[3], hmv[3];
+    int bgv[KS];
+    double tsv[KS], hmv[KS];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < KS; ++k) {
       const int i = lane + 32 * k;
       const int64_t gi = g + i;
       bgv[k] = (i <= nb + 1 && gi <= a.n_seg) ? a.begins[gi] : INT_MAX;
-      tsv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? sqrt((double)a.tail_count[gi]) : 1.0;
+      tsv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? fast_sqrt_d((double)a.tail_count[gi]) : 1.0;
       hmv[k] = (a.head_mul && i <= nb && gi < a.n_seg) ? a.head_mul[gi] : 1.0;
     }
     if (w > 0) stage_rows<SLOTS, VEC, VJ>(a, geo, sm, pb, nb, lane);
@@ -353,10 +387,10 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
     // Group starts inside the batch (groups g+1 .. g+nb can start here):
     // flagged in shared memory, then each row's group is g plus a ballot
     // prefix count.
-    for (int i = lane; i < kMaxRB; i += 32) sm.startf[i] = 0;
+    for (int i = lane; i < (CW && !FUSED ? kRbC : kMaxRB); i += 32) sm.startf[i] = 0;
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < KS; ++k) {
       const int i = lane + 32 * k - 1;  // group g + 1 + i starts at bgv[k]
       if (i >= 0 && i < nb && g + 1 + i < a.n_seg) {
         const int64_t b = bgv[k];
@@ -366,22 +400,31 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
     __syncwarp();
     // begins[g + i] and the tail scale of group g + i from the registers.
     auto bg_at = [&](int i) -> int64_t {
-      const int v0 = __shfl_sync(0xffffffffu, bgv[0], i & 31);
-      const int v1 = __shfl_sync(0xffffffffu, bgv[1], i & 31);
-      const int v2 = __shfl_sync(0xffffffffu, bgv[2], i & 31);
-      return i < 32 ? v0 : (i < 64 ? v1 : v2);
+      int v = __shfl_sync(0xffffffffu, bgv[0], i & 31);
+#pragma unroll
+      for (int k = 1; k < KS; ++k) {
+        const int vk = __shfl_sync(0xffffffffu, bgv[k], i & 31);
+        if ((i >> 5) == k) v = vk;
+      }
+      return v;
     };
     auto ts_at = [&](int i) -> double {
-      const double v0 = __shfl_sync(0xffffffffu, tsv[0], i & 31);
-      const double v1 = __shfl_sync(0xffffffffu, tsv[1], i & 31);
-      const double v2 = __shfl_sync(0xffffffffu, tsv[2], i & 31);
-      return i < 32 ? v0 : (i < 64 ? v1 : v2);
+      double v = __shfl_sync(0xffffffffu, tsv[0], i & 31);
+#pragma unroll
+      for (int k = 1; k < KS; ++k) {
+        const double vk = __shfl_sync(0xffffffffu, tsv[k], i & 31);
+        if ((i >> 5) == k) v = vk;
+      }
+      return v;
     };
     auto hm_at = [&](int i) -> double {
-      const double v0 = __shfl_sync(0xffffffffu, hmv[0], i & 31);
-      const double v1 = __shfl_sync(0xffffffffu, hmv[1], i & 31);
-      const double v2 = __shfl_sync(0xffffffffu, hmv[2], i & 31);
-      return i < 32 ? v0 : (i < 64 ? v1 : v2);
+      double v = __shfl_sync(0xffffffffu, hmv[0], i & 31);
+#pragma unroll
+      for (int k = 1; k < KS; ++k) {
+        const double vk = __shfl_sync(0xffffffffu, hmv[k], i & 31);
+        if ((i >> 5) == k) v = vk;
+      }
+      return v;
     };
     int64_t gcur = g;
     // Row metadata and coefficients, one row per lane.
@@ -440,16 +483,34 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         const double incl = x;
         const double prev = __shfl_up_sync(0xffffffffu, incl, 1);
         const double excl = (fl & 1) ? 0.0 : (lane == 0 ? N : prev);
+        // sqrt(excl)/sqrt(incl) and 1/(sqrt(excl) sqrt(incl)) from one
+        // rsqrt of the product (MUFU + two Newton steps, ~1e-16) inside a
+        // range where neither the product nor the .ftz approximation can
+        // flush; the IEEE sqrt/div sequences (about 6 x 35 instructions per
+        // row) only outside it.
+        const double pq = excl * incl;
+        const bool fast = pq > 1e-250 && pq < 1e250 && incl > 1e-250 && incl < 1e250;
         if (live && jj >= 1) {
-          const double np_ = sqrt(excl);
-          const double nn = sqrt(incl);
-          al = np_ / nn * ts;
-          be = v / (np_ * nn) * ts;
+          if (fast) {
+            const double rq = fast_rsqrt_d(pq);
+            al = excl * rq * ts;
+            be = v * rq * ts;
+          } else {
+            const double np_ = sqrt(excl);
+            const double nn = sqrt(incl);
+            al = np_ / nn * ts;
+            be = v / (np_ * nn) * ts;
+          }
         }
         if (live && (fl & 2)) {
-          const double nrm = sqrt(incl);
-          hc = 1.0 / nrm;
-          sc = nrm;
+          if (incl > 1e-250 && incl < 1e250) {
+            hc = fast_rsqrt_d(incl);
+            sc = incl * hc;
+          } else {
+            const double nrm = sqrt(incl);
+            hc = 1.0 / nrm;
+            sc = nrm;
+          }
         }
         const int last_lane = min(31, nb - base - 1);
         N = __shfl_sync(0xffffffffu, incl, last_lane);
@@ -461,10 +522,18 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         sm.hco[rr] = hc * hmr;
         sm.wt[rr] = weighted ? v : sc;  // plain rows never read their weight
         sm.segfl[rr] = make_int2((int)sg, fl);
-        if ((fl & 2) && a.scales && a.wj < 0) {
+        // Output rows of the emission pass, computed once per row here
+        // instead of once per lane there (64-bit index arithmetic).
+        const int64_t p = pb + rr;
+        sm.rowptr[rr] = (a.tails && !(fl & 1)) ? a.tails + (p - sg - 1) * a.ldt : nullptr;
+        double* hp = nullptr;
+        if (fl & 2) {
           const int64_t hi = a.head_index ? a.head_index[sg] : sg;
-          a.scales[hi] = a.scale_count ? sqrt((double)a.scale_count[sg]) : sc;
+          if (a.heads) hp = a.heads + hi * a.ldh;
+          if (a.scales && a.wj < 0)
+            a.scales[hi] = a.scale_count ? sqrt((double)a.scale_count[sg]) : sc;
         }
+        sm.hrowp[rr] = hp;
       }
     }
     if (w > 0) __pipeline_wait_prior(0);
@@ -542,16 +611,9 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
         const int2 sf = sm.segfl[rr];
         const double2 cf = sm.coef[rr];
         const double vw = sm.wt[rr];
-        const int64_t p = pb + rr;
-        double* trow = (a.tails && !(sf.y & 1)) ? a.tails + (p - sf.x - 1) * a.ldt
-                                               : nullptr;
-        double* hrow = nullptr;
-        double hc = 0.0;
-        if ((sf.y & 2) && a.heads) {
-          const int64_t hi = a.head_index ? a.head_index[sf.x] : sf.x;
-          hrow = a.heads + hi * a.ldh;
-          hc = sm.hco[rr];
-        }
+        double* trow = const_cast<double*>(sm.rowptr[rr]);
+        double* hrow = sm.hrowp[rr];
+        const double hc = hrow ? sm.hco[rr] : 0.0;
         const double* row = sm.buf + rr * geo.ls;
         // Join-on-write factors of this group (process_and_join_children,
         // figaro.hpp:196-230, in its product order).
@@ -663,8 +725,8 @@ __device__ void process_unit(const HtDev& a, const Geo& geo, SM& sm,
   }
 }
 
-template <int SLOTS, int VEC, bool VJ, bool JW = false>
-__global__ void __launch_bounds__(kWarps * 32)
+template <int SLOTS, int VEC, bool VJ, bool JW = false, int CW = 0>
+__global__ void __launch_bounds__(kWarps * 32, (VJ || JW || SLOTS > 1) ? 1 : FG_HT_MINB)
     k_heads_tails(HtDev a, Geo geo) {
   using SMT = std::conditional_t<VJ, WarpSmemVJ, WarpSmem>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -678,7 +740,12 @@ __global__ void __launch_bounds__(kWarps * 32)
     if (lane == 0) u = atomicAdd(a.ticket, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= a.n_units) break;
-    process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW>(a, geo, sm, u, lane, dummy);
+    if constexpr (CW > 0) {
+      const GeoC<CW> gc{};
+      process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW, GeoC<CW>>(a, gc, sm, u, lane, dummy);
+    } else {
+      process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW>(a, geo, sm, u, lane, dummy);
+    }
   }
 }
 
@@ -1026,6 +1093,10 @@ __global__ void __launch_bounds__(256) k_join_elems2(const __grid_constant__ Joi
 // double2 elements are written with a fixed (row, packet) split per thread
 // -- no factor array in HBM, no per-element division.
 constexpr int kJoinMaxC = 4;
+#ifndef FG_JOIN_UNROLL
+#define FG_JOIN_UNROLL 11
+#endif
+constexpr int kJoinUnroll = FG_JOIN_UNROLL;
 __global__ void __launch_bounds__(kJoinTile) k_join_tile(const __grid_constant__ JoinArgs a) {
   __shared__ double fs[kJoinTile][kJoinMaxC + 1];  // child factors, [nc] = all
   __shared__ int is[kJoinTile][kJoinMaxC];
@@ -1069,7 +1140,7 @@ __global__ void __launch_bounds__(kJoinTile) k_join_tile(const __grid_constant__
     }
     __syncthreads();
     if (tr < rpp) {
-#pragma unroll 4
+#pragma unroll kJoinUnroll
       for (int r = tr; r < rows; r += rpp) {
         double2* dst = reinterpret_cast<double2*>(a.S + (k0 + r) * a.width) + tp;
         if (j < a.own_w) {
@@ -1097,10 +1168,10 @@ __global__ void __launch_bounds__(kJoinTile) k_join_tile(const __grid_constant__
   }
 }
 
-template <int SLOTS, int VEC, bool VJ, bool JW = false>
+template <int SLOTS, int VEC, bool VJ, bool JW = false, int CW = 0>
 void launch_main(Context& ctx, const HtDev& d, const Geo& geo) {
   const size_t smem = (VJ ? sizeof(WarpSmemVJ) : sizeof(WarpSmem)) * kWarps;
-  auto kern = k_heads_tails<SLOTS, VEC, VJ, JW>;
+  auto kern = k_heads_tails<SLOTS, VEC, VJ, JW, CW>;
   FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   int per_sm = 0;
@@ -1130,6 +1201,22 @@ void launch_slots(Context& ctx, const HtDev& d, const Geo& geo) {
     if (slots <= 1) launch_main<1, VEC, false, true>(ctx, d, geo);
     else launch_main<2, VEC, false, true>(ctx, d, geo);
     return;
+  }
+  // Hot shapes with compile-time geometry (C3: own F width 8, project-away
+  // width 20; C4: widths 4, 8, 12; 16 for two-relation joins).
+  if constexpr (VEC == 2) {
+    const bool exact = slots <= 1 && geo.L == geo.np && geo.G == 32 / geo.np &&
+                       geo.ls == d.w && d.w == 2 * geo.np && getenv("FG_HT_RUNTIME_GEO") == nullptr;
+    if (exact) {
+      switch (d.w) {
+        case 4: return launch_main<1, 2, false, false, 4>(ctx, d, geo);
+        case 8: return launch_main<1, 2, false, false, 8>(ctx, d, geo);
+        case 12: return launch_main<1, 2, false, false, 12>(ctx, d, geo);
+        case 16: return launch_main<1, 2, false, false, 16>(ctx, d, geo);
+        case 20: return launch_main<1, 2, false, false, 20>(ctx, d, geo);
+        default: break;
+      }
+    }
   }
   if (slots <= 1) launch_main<1, VEC, false>(ctx, d, geo);
   else if (slots <= 2) launch_main<2, VEC, false>(ctx, d, geo);
@@ -1332,7 +1419,10 @@ void run_heads_tails(Context& ctx, const HeadTailArgs& in) {
 namespace {
 using FW4 = WCfg<4, 1, 8, 2>;
 using FW8 = WCfg<8, 2, 8, 2>;
-using FW16 = WCfg<16, 4, 8, 2>;
+#ifndef FG_FW16_RPT
+#define FG_FW16_RPT 8
+#endif
+using FW16 = WCfg<16, 4, FG_FW16_RPT, 2>;
 using FW16r = WCfg<16, 4, 8, 2, 1>;
 using FW32 = WCfg<32, 4, 8, 1>;
 using FW12 = WCfg<12, 3, 8, 2>;

@@ -495,7 +495,10 @@ __device__ __forceinline__ unsigned long long warp_look_back(unsigned long long*
 
 // ------------------------------------------------------- segment extraction
 
-constexpr int kSegIpt = 16;
+#ifndef FG_SEG_IPT
+#define FG_SEG_IPT 8
+#endif
+constexpr int kSegIpt = FG_SEG_IPT;
 constexpr int kSegTile = kSortThreads * kSegIpt;
 
 template <class KeyT>
