@@ -422,7 +422,11 @@ void launch_fjs(Context& ctx, const uint64_t* sizes, const uint64_t* theta,
     return std::string(e) == "peers" ? 1 : 2;
   }();
   auto launch = [&](auto kern, int c) {
-    const int grid = (int)std::min<int64_t>(ctx.sm_count * 4, ceil_div(G, kThreads));
+    static const int per_sm = [] {
+      const char* e = getenv("FG_SCATTER_GRID");
+      return e ? std::max(1, atoi(e)) : 4;
+    }();
+    const int grid = (int)std::min<int64_t>((int64_t)ctx.sm_count * per_sm, ceil_div(G, kThreads));
     kern<<<std::max(grid, 1), kThreads, 0, ctx.stream>>>(fjs, G, ch.lidx[c], ch.phi_up[c],
                                                           child_P[c], status);
     FG_LAUNCHED(ctx);

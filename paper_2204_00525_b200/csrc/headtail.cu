@@ -42,6 +42,10 @@ namespace fg {
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
+#ifndef FG_FUSED_WARPS
+#define FG_FUSED_WARPS 8
+#endif
+constexpr int kFusedWarps = FG_FUSED_WARPS;  // warps per CTA of the fused kernel
 constexpr int kUnit = 256;           // rows per work unit
 constexpr int kLight = 256;          // groups up to this size recompute carries
 #ifndef FG_HT_SMEM
@@ -84,6 +88,7 @@ struct HtDev {
   const int* ufirst;     // per unit: group of its first row (or null)
   const int64_t* qb;     // per unit: its first row (n_units + 1 entries, or null)
   const double* head_mul;  // per group: heads *= head_mul[g] (or null)
+  int l2hint;              // 1: L2::64B fetch hint for permuted short rows (cp_async)
   // Join-on-read (K4 folded into K5; process_and_join_children,
   // figaro.hpp:196-230): with nj >= 0 the data row x is never materialised;
   // it is [jhead[x, :own_w] * all | jS[c][jlidx[c][x]] * f_c ...] with
@@ -238,16 +243,34 @@ struct GeoC {
 template <class GEO> struct GeoW { static constexpr int value = GEO::kW; };
 template <> struct GeoW<Geo> { static constexpr int value = 0; };
 
+// Asynchronous copy of one packet into shared memory with the L2::64B
+// fetch hint: without it a miss fills the whole 128-byte line, so gathering
+// 64-byte rows through the sort permutation reads every row twice from HBM
+// (scripts/gather_probe.cu: 6.53 GB vs 3.41 GB of DRAM reads for 3.2 GB of
+// rows).  Only for permuted rows shorter than a line (`narrow`): on
+// contiguous or long rows the hint costs the line's second half a second
+// request (measured: C3 project-away and C5 own rows slower with it).
 template <int VEC>
-__device__ __forceinline__ void cp_async(double* dst, const double* src) {
-  __pipeline_memcpy_async(dst, src, VEC * sizeof(double));
+__device__ __forceinline__ void cp_async(double* dst, const double* src, bool narrow = false) {
+  if (narrow) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if (VEC == 2)
+      asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(d), "l"(src));
+    else
+      asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(d), "l"(src));
+  } else {
+    __pipeline_memcpy_async(dst, src, VEC * sizeof(double));
+  }
 }
 
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
-template <int SLOTS, int VEC, bool VJ, class SM, class GEO>
+// pv (KP > 0): the batch's permutation entries, row lane + 32 k in pv[k],
+// loaded one batch ahead by the caller so the row gathers do not wait on a
+// dependent index load.
+template <int SLOTS, int VEC, bool VJ, class SM, class GEO, int KP = 0>
 __device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
                                            SM& sm, int64_t p, int nb,
-                                           int lane) {
+                                           int lane, const int* pv = nullptr) {
   if constexpr (VJ) {
     // Join-on-read: own head columns and child summary rows are copied into
     // the row buffer; the row factors are applied when the buffer is read.
@@ -282,20 +305,33 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
     __pipeline_commit();
     return;
   }
-  for (int rr = lane; rr < nb; rr += 32) {
-    const int64_t x = src_row(a, p + rr);
-    sm.rowptr[rr] = a.data + x * a.ld;
-    if (a.weights) sm.wt[rr] = a.weights[x];
+  if constexpr (KP > 0) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int rr = lane + 32 * k;
+      if (rr < nb) {
+        const int64_t x = a.perm ? (int64_t)pv[k] : p + rr;
+        sm.rowptr[rr] = a.data + x * a.ld;
+        if (a.weights) sm.wt[rr] = a.weights[x];
+      }
+    }
+  } else {
+    for (int rr = lane; rr < nb; rr += 32) {
+      const int64_t x = src_row(a, p + rr);
+      sm.rowptr[rr] = a.data + x * a.ld;
+      if (a.weights) sm.wt[rr] = a.weights[x];
+    }
   }
   __syncwarp();
   const int g = lane / geo.L, cl = lane % geo.L;
+  const bool narrow = a.perm != nullptr && a.w < 16 && a.l2hint;
   for (int rr = g < geo.G ? g : nb; rr < nb; rr += geo.G) {
     const double* src = sm.rowptr[rr];
     double* dst = sm.buf + rr * geo.ls;
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
       const int pk = cl + geo.L * s;
-      if (pk < geo.np) cp_async<VEC>(dst + VEC * pk, src + VEC * pk);
+      if (pk < geo.np) cp_async<VEC>(dst + VEC * pk, src + VEC * pk, narrow);
     }
   }
   __pipeline_commit();
@@ -366,8 +402,27 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
                           : 0;
   constexpr int KS = (CW && !FUSED) ? (kRbC + 1) / 32 + 1 : 3;
   const int rbv = (CW && !FUSED) ? kRbC : a.rb;
+  // Permutation entries of the next batch, loaded one batch ahead.
+  constexpr int KP = (CW && !FUSED && !VJ) ? (kRbC + 31) / 32 : 0;
+  int pnext[KP > 0 ? KP : 1];
+  if constexpr (KP > 0) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int64_t pr = q0 + lane + 32 * k;
+      pnext[k] = (a.perm && pr < q1) ? a.perm[pr] : 0;
+    }
+  }
   for (int64_t pb = q0; pb < q1; pb += rbv) {
     const int nb = (int)(q1 - pb < (int64_t)rbv ? q1 - pb : (int64_t)rbv);
+    int pcur[KP > 0 ? KP : 1];
+    if constexpr (KP > 0) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        pcur[k] = pnext[k];
+        const int64_t pr = pb + rbv + lane + 32 * k;
+        pnext[k] = (a.perm && lane + 32 * k < rbv && pr < q1) ? a.perm[pr] : 0;
+      }
+    }
     // The batch's rows lie in groups g .. g+nb: their offsets begins[g ..
     // g+nb+1] and tail scales sqrt(tail_count[g .. g+nb]) are loaded now,
     // three per lane in registers, so their latency overlaps the row
@@ -382,7 +437,7 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
       tsv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? fast_sqrt_d((double)a.tail_count[gi]) : 1.0;
       hmv[k] = (a.head_mul && i <= nb && gi < a.n_seg) ? a.head_mul[gi] : 1.0;
     }
-    if (w > 0) stage_rows<SLOTS, VEC, VJ>(a, geo, sm, pb, nb, lane);
+    if (w > 0) stage_rows<SLOTS, VEC, VJ, SM, GEO, KP>(a, geo, sm, pb, nb, lane, pcur);
     else if (VJ) __syncwarp();
     // Group starts inside the batch (groups g+1 .. g+nb can start here):
     // flagged in shared memory, then each row's group is g plus a ballot
@@ -673,9 +728,12 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
             if (jwrite) {
 #pragma unroll
               for (int e = 0; e < VEC; ++e) hrow[VEC * pk + e] = (run[s][e] * hc) * jall;
+            } else if (VEC == 2) {
+              // one 16-byte store (prepare() checks the alignment of heads / ldh)
+              *reinterpret_cast<double2*>(hrow + 2 * pk) =
+                  make_double2(run[s][0] * hc, run[s][VEC - 1] * hc);
             } else {
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) hrow[VEC * pk + e] = run[s][e] * hc;
+              hrow[pk] = run[s][0] * hc;
             }
           }
         }
@@ -753,7 +811,7 @@ __global__ void __launch_bounds__(kWarps * 32, (VJ || JW || SLOTS > 1) ? 1 : FG_
 // per-warp Householder accumulator (never written to HBM).  Writes one
 // F::W x F::W partial factor per warp to `partials`.
 template <int VEC, class F>
-__global__ void __launch_bounds__(kWarps * 32, F::MINB)
+__global__ void __launch_bounds__(kFusedWarps * 32, F::MINB)
     k_heads_tails_tsqr(HtDev a, Geo geo, double* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using SM = WarpSmemT<kFusedDoubles>;
@@ -768,11 +826,11 @@ __global__ void __launch_bounds__(kWarps * 32, F::MINB)
     for (int q = 0; q < F::CPT; ++q) Racc[m][q] = 0.0;
   // Static unit -> warp assignment: which rows each accumulator absorbs
   // (and so the rounding of R) depends only on the grid, not on timing.
-  const int64_t nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t u = (int64_t)blockIdx.x * kWarps + warp; u < a.n_units; u += nw)
+  const int64_t nw = (int64_t)gridDim.x * kFusedWarps;
+  for (int64_t u = (int64_t)blockIdx.x * kFusedWarps + warp; u < a.n_units; u += nw)
     process_unit<1, VEC, F, false>(a, geo, sm, u, lane, Racc);
   const int r = lane % F::TR, c = lane / F::TR;
-  double* o = partials + ((int64_t)blockIdx.x * kWarps + warp) * F::W * F::W;
+  double* o = partials + ((int64_t)blockIdx.x * kFusedWarps + warp) * F::W * F::W;
 #pragma unroll
   for (int m = 0; m < F::RR; ++m)
 #pragma unroll
@@ -1269,6 +1327,7 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   d.ldt = in.ldt;
   d.scales = in.scales;
   d.head_mul = in.head_mul;
+  d.l2hint = getenv("FG_NO_L2_HINT") == nullptr;
   d.nj = -1;
   d.wj = -1;
   if (in.join_write) {
@@ -1374,7 +1433,9 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
                                     reinterpret_cast<uintptr_t>(in.data) % 16 == 0;
   const bool aligned = in.w > 0 && in.w % 2 == 0 && src_ok &&
                        (!in.tails || (in.ldt % 2 == 0 &&
-                                      reinterpret_cast<uintptr_t>(in.tails) % 16 == 0));
+                                      reinterpret_cast<uintptr_t>(in.tails) % 16 == 0)) &&
+                       (!in.heads || in.join_write ||
+                        (in.ldh % 2 == 0 && reinterpret_cast<uintptr_t>(in.heads) % 16 == 0));
   geo.vec = aligned ? 2 : 1;
   geo.np = in.w > 0 ? (in.w + geo.vec - 1) / geo.vec : 1;
   geo.L = 1;
@@ -1432,20 +1493,20 @@ using FW24 = WCfg<24, 3, 8, 1>;
 template <int VEC, class F>
 int launch_fused(Context& ctx, HtPrep& P, DevArray<double>& partials) {
   using SM = WarpSmemT<kFusedDoubles>;
-  const size_t smem = sizeof(SM) * kWarps;
+  const size_t smem = sizeof(SM) * kFusedWarps;
   auto kern = k_heads_tails_tsqr<VEC, F>;
   FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   int per_sm = 0;
   FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
-                                                        kWarps * 32, smem));
+                                                        kFusedWarps * 32, smem));
   int64_t grid = (int64_t)ctx.sm_count * std::max(per_sm, 1);
-  grid = std::max<int64_t>(1, std::min<int64_t>(grid, ceil_div(P.d.n_units, kWarps)));
-  partials.alloc((size_t)grid * kWarps * F::W * F::W, ctx.stream);
-  kern<<<(int)grid, kWarps * 32, smem, ctx.stream>>>(P.d, P.geo, partials.get());
+  grid = std::max<int64_t>(1, std::min<int64_t>(grid, ceil_div(P.d.n_units, kFusedWarps)));
+  partials.alloc((size_t)grid * kFusedWarps * F::W * F::W, ctx.stream);
+  kern<<<(int)grid, kFusedWarps * 32, smem, ctx.stream>>>(P.d, P.geo, partials.get());
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
-  return (int)(grid * kWarps);
+  return (int)(grid * kFusedWarps);
 }
 
 template <class F>

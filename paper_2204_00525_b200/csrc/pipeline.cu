@@ -11,6 +11,7 @@
 //   postprocess_thin + normalize_signs     -> K6/K7 (tsqr.cu)
 // Device phases are timed with CUDA events on the context stream.
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <climits>
 #include <cstdlib>
@@ -943,6 +944,15 @@ fg_status fg_ctx_create(int32_t device, fg_ctx** out) {
     }
     ctx->sm_count = prop.multiProcessorCount;
     ctx->smem_optin = prop.sharedMemPerBlockOptin;
+    // FG_L2_FETCH=32|64|128: L2 fetch granularity hint (experiments with the
+    // permuted 64-byte row gathers); the device default otherwise.
+    if (const char* e = getenv("FG_L2_FETCH")) {
+      size_t before = 0, after = 0;
+      cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
+      cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
+      cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
+      fprintf(stderr, "[fg] L2 fetch granularity %zu -> %zu\n", before, after);
+    }
     FG_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
     ctx->stream = ctx->own;
     FG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
