@@ -115,7 +115,9 @@ __device__ __forceinline__ uint64_t project_one(uint64_t k,
 }
 
 __global__ void k_project(const uint64_t* __restrict__ in, int64_t n,
-                          PackSpec s, uint64_t* __restrict__ out) {
+                          PackSpec s, uint64_t* __restrict__ out,
+                          const int64_t* __restrict__ n_dev) {
+  if (n_dev) n = *n_dev;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = project_one(in[i], s);
@@ -222,9 +224,9 @@ void launch_pack_keys(Context& ctx, const int64_t* keys, int64_t rows,
 }
 
 void launch_project(Context& ctx, const uint64_t* in, int64_t n,
-                    const PackSpec& s, uint64_t* out) {
+                    const PackSpec& s, uint64_t* out, const int64_t* n_dev) {
   if (n == 0) return;
-  k_project<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(in, n, s, out);
+  k_project<<<grid_for(ctx, n), kThreads, 0, ctx.stream>>>(in, n, s, out, n_dev);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
 }
@@ -337,14 +339,14 @@ void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
 
 void group_begin_presorted(Context& ctx, const uint64_t* keys, int64_t n,
                            const int* perm_in, GroupOut& out, GroupPending& pend,
-                           int* pidx) {
+                           int* pidx, const int64_t* n_dev, bool want_perm) {
   cudaStream_t st = ctx.stream;
-  out.perm.alloc(n, st);
+  if (want_perm) out.perm.alloc(n, st);
   pend.n = n;
   pend.begins.alloc(n + 1, st);
   pend.uniq.alloc(n, st);
   pend.nr.alloc(1, st);
-  if (n) {
+  if (n && want_perm) {
     if (perm_in)
       FG_CUDA(cudaMemcpyAsync(out.perm.get(), perm_in, n * sizeof(int),
                               cudaMemcpyDeviceToDevice, st));
@@ -352,7 +354,7 @@ void group_begin_presorted(Context& ctx, const uint64_t* keys, int64_t n,
       launch_iota(ctx, out.perm.get(), n);
   }
   launch_segments<uint64_t>(ctx, keys, n, pend.begins.get(), pend.uniq.get(), pend.nr.get(),
-                            perm_in, pidx);
+                            perm_in, pidx, n_dev);
 }
 
 template <class KeyT>

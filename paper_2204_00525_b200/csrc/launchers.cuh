@@ -29,8 +29,10 @@ template <class KeyT>
 void launch_pack_keys(Context& ctx, const int64_t* keys, int64_t rows,
                       int n_key, const PackSpec& spec, KeyT* out, int* iota);
 // Re-packs already packed keys into another field layout (projection).
+// n_dev (optional): the real element count, device-resident; n is then the
+// host's upper bound (grid sizing only).
 void launch_project(Context& ctx, const uint64_t* in, int64_t n,
-                    const PackSpec& from_to, uint64_t* out);
+                    const PackSpec& from_to, uint64_t* out, const int64_t* n_dev = nullptr);
 // Stable radix sort of (key, perm) on the low `bits` bits + segment
 // extraction.  perm_in == null means the identity permutation.
 struct GroupOut {
@@ -62,9 +64,12 @@ void group_begin32(Context& ctx, const uint32_t* keys, int64_t n, int bits,
                    const uint32_t* hist = nullptr, int* pidx = nullptr);
 void group_finish(Context& ctx, int64_t G, GroupOut& out, GroupPending& pend);
 // Same for keys already in ascending order (no sort; perm_in is kept).
+// n_dev: as launch_project (buffers are sized for n); want_perm = false
+// skips the (identity) permutation output.
 void group_begin_presorted(Context& ctx, const uint64_t* keys, int64_t n,
                            const int* perm_in, GroupOut& out, GroupPending& pend,
-                           int* pidx = nullptr);
+                           int* pidx = nullptr, const int64_t* n_dev = nullptr,
+                           bool want_perm = true);
 void exclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
 void inclusive_sum_int(Context& ctx, const int* in, int* out, int64_t n);
 
@@ -84,7 +89,8 @@ void radix_sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out, const i
 // *n_runs = G (device); pidx[perm ? perm[p] : p] = run of position p.
 template <class KeyT>
 void launch_segments(Context& ctx, const KeyT* sorted, int64_t n, int* begins, uint64_t* uniq,
-                     int64_t* n_runs, const int* perm, int* pidx);
+                     int64_t* n_runs, const int* perm, int* pidx,
+                     const int64_t* n_dev = nullptr);
 void scan_int(Context& ctx, const int* in, int* out, int64_t n, bool inclusive);
 // out[0..*count) = in[i] for keep[i] != 0, in order (device count).
 void compact_flagged(Context& ctx, const int* in, const char* keep, int* out, int64_t n,

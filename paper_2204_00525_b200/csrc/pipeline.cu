@@ -193,11 +193,11 @@ void check_nonempty(const NodeState& n) {
 
 // --------------------------------------------------------------- status
 
-void check_status(Context& ctx, const char* phase) {
-  unsigned st = 0;
-  FG_CUDA(cudaMemcpyAsync(&st, ctx.status.get(), sizeof st,
-                          cudaMemcpyDeviceToHost, ctx.stream));
-  sync_stream(ctx);
+// Maps the device status word read back with the final synchronisation to
+// the reference's exceptions.  The transform and TSQR kernels tolerate the
+// flagged states (a missing child is a zero row, inexact counts are 0), so
+// the word is read once at the end instead of stalling the stream after K2.
+void raise_status(unsigned st, const char* phase) {
   if (!st) return;
   const std::string p = phase;
   if (st & ST_MISSING_CHILD)
@@ -448,83 +448,99 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
       group_begin(ctx, pk64[ni].get(), n.rows, n.own_bits, n.sel.get(), n.grp, pend[ni]);
     }
   }
-  {
-    std::vector<int64_t> Gs(nodes.size(), 0);
-    for (size_t ni = 0; ni < nodes.size(); ++ni)
-      FG_CUDA(cudaMemcpyAsync(&Gs[ni], pend[ni].nr.get(), sizeof(int64_t),
-                              cudaMemcpyDeviceToHost, st));
-    sync_stream(ctx);
-    for (size_t ni = 0; ni < nodes.size(); ++ni) {
-      NodeState& n = *nodes[ni];
-      group_finish(ctx, Gs[ni], n.grp, pend[ni]);
-      pk32[ni].release();
-      pk64[ni].release();
-      hists[ni].release();
-      n.sizes.alloc(n.grp.G, st);
-      launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
+  // Parent-key grouping of own segments (the std::map regroupings of
+  // counts.hpp:121-130 and figaro.hpp:236-239).  Parent attributes that are
+  // the leading own-key attributes (in the same order) project the ascending
+  // own keys to ascending parent keys -- no sort (C3's F under D1, C4's R2
+  // under R1, every leaf, 2-way joins): those regroupings are enqueued right
+  // behind the own grouping with the group count G still on the device, so
+  // one synchronisation reads every G and P.  Other nodes sort their G
+  // projected keys after it (a second synchronisation for their P).
+  std::vector<GroupPending> ppend(nodes.size());
+  std::vector<GroupOut> pgs(nodes.size());
+  std::vector<DevArray<uint64_t>> ppks(nodes.size());
+  auto parent_spec = [&](NodeState& n, int* pbits) {
+    n.par = make_spec(n.pattr, code,
+                      [&](int a) {
+                        const int f = (int)(std::find(n.key_attr.begin(),
+                                                      n.key_attr.end(), a) -
+                                            n.key_attr.begin());
+                        return n.own.shift[f];
+                      },
+                      pbits, "relation " + n.name + " (parent key)");
+  };
+  bool any_sorted_parent = false;
+  for (size_t ni = 0; ni < nodes.size(); ++ni) {
+    NodeState& n = *nodes[ni];
+    if (n.parent < 0) continue;
+    const bool prefix = n.pattr.size() <= n.key_attr.size() &&
+                        std::equal(n.pattr.begin(), n.pattr.end(), n.key_attr.begin());
+    n.pa_identity = prefix;
+    if (!prefix) {
+      any_sorted_parent = true;
+      continue;
     }
+    int pbits = 0;
+    parent_spec(n, &pbits);
+    // upper bound: G <= rows
+    ppks[ni].alloc(n.rows, st);
+    n.pidx.alloc(n.rows, st);
+    launch_project(ctx, pend[ni].uniq.get(), n.rows, n.par, ppks[ni].get(), pend[ni].nr.get());
+    // pidx[g] = parent-key run of own segment g, written by the segment
+    // extraction of the parent-key grouping.
+    group_begin_presorted(ctx, ppks[ni].get(), n.rows, nullptr, pgs[ni], ppend[ni],
+                          n.pidx.get(), pend[ni].nr.get(), /*want_perm=*/false);
+  }
+  std::vector<int64_t> Gs(nodes.size(), 0), Ps(nodes.size(), 0);
+  for (size_t ni = 0; ni < nodes.size(); ++ni) {
+    FG_CUDA(cudaMemcpyAsync(&Gs[ni], pend[ni].nr.get(), sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, st));
+    if (nodes[ni]->parent >= 0 && nodes[ni]->pa_identity)
+      FG_CUDA(cudaMemcpyAsync(&Ps[ni], ppend[ni].nr.get(), sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+  }
+  sync_stream(ctx);
+  for (size_t ni = 0; ni < nodes.size(); ++ni) {
+    NodeState& n = *nodes[ni];
+    group_finish(ctx, Gs[ni], n.grp, pend[ni]);
+    pk32[ni].release();
+    pk64[ni].release();
+    hists[ni].release();
+    n.sizes.alloc(n.grp.G, st);
+    launch_seg_sizes(ctx, n.grp.begins.get(), n.grp.G, n.sizes.get());
   }
   tr.mark("own grouping");
-  // Parent-key grouping of own segments (the std::map regroupings of
-  // counts.hpp:121-130 and figaro.hpp:236-239), batched like K1.
-  {
-    std::vector<GroupPending> ppend(nodes.size());
-    std::vector<GroupOut> pgs(nodes.size());
-    std::vector<DevArray<uint64_t>> ppks(nodes.size());
+  if (any_sorted_parent) {
     for (size_t ni = 0; ni < nodes.size(); ++ni) {
       NodeState& n = *nodes[ni];
-      if (n.parent < 0) continue;
+      if (n.parent < 0 || n.pa_identity) continue;
       int pbits = 0;
-      n.par = make_spec(n.pattr, code,
-                        [&](int a) {
-                          const int f = (int)(std::find(n.key_attr.begin(),
-                                                        n.key_attr.end(), a) -
-                                              n.key_attr.begin());
-                          return n.own.shift[f];
-                        },
-                        &pbits, "relation " + n.name + " (parent key)");
+      parent_spec(n, &pbits);
       const int64_t G = n.grp.G;
       ppks[ni].alloc(G, st);
       launch_project(ctx, n.grp.uniq.get(), G, n.par, ppks[ni].get());
-      // pidx[g] = parent-key run of own segment g, written by the segment
-      // extraction of the parent-key grouping.
       n.pidx.alloc(G, st);
-      // Parent attributes that are the leading own-key attributes (in the
-      // same order) project the ascending own keys to ascending parent
-      // keys: no sort needed (C3's F under D1, C4's R2 under R1, 2-way joins).
-      const bool prefix = n.pattr.size() <= n.key_attr.size() &&
-                          std::equal(n.pattr.begin(), n.pattr.end(), n.key_attr.begin());
-      n.pa_identity = prefix;
-      if (prefix)
-        group_begin_presorted(ctx, ppks[ni].get(), G, nullptr, pgs[ni], ppend[ni],
-                              n.pidx.get());
-      else
-        group_begin(ctx, ppks[ni].get(), G, pbits, nullptr, pgs[ni], ppend[ni], nullptr,
-                    n.pidx.get());
+      group_begin(ctx, ppks[ni].get(), G, pbits, nullptr, pgs[ni], ppend[ni], nullptr,
+                  n.pidx.get());
+      FG_CUDA(cudaMemcpyAsync(&Ps[ni], ppend[ni].nr.get(), sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
     }
-    std::vector<int64_t> Ps(nodes.size(), 0);
-    bool any = false;
-    for (size_t ni = 0; ni < nodes.size(); ++ni)
-      if (nodes[ni]->parent >= 0) {
-        FG_CUDA(cudaMemcpyAsync(&Ps[ni], ppend[ni].nr.get(), sizeof(int64_t),
-                                cudaMemcpyDeviceToHost, st));
-        any = true;
-      }
-    if (any) sync_stream(ctx);
-    for (size_t ni = 0; ni < nodes.size(); ++ni) {
-      NodeState& n = *nodes[ni];
-      if (n.parent < 0) continue;
-      const int64_t G = n.grp.G;
-      GroupOut& pg = pgs[ni];
-      group_finish(ctx, Ps[ni], pg, ppend[ni]);
-      n.P = pg.G;
-      n.pa_perm = std::move(pg.perm);
-      n.pa_begins = std::move(pg.begins);
-      n.upk = std::move(pg.uniq);
-      if (n.children.empty() && n.P != G)
-        fail(FG_E_INTEGRITY, "relation " + n.name +
-                                 ": leaf keys do not match its parent attributes");
-    }
+    sync_stream(ctx);
+  }
+  for (size_t ni = 0; ni < nodes.size(); ++ni) {
+    NodeState& n = *nodes[ni];
+    if (n.parent < 0) continue;
+    const int64_t G = n.grp.G;
+    GroupOut& pg = pgs[ni];
+    group_finish(ctx, Ps[ni], pg, ppend[ni]);
+    n.P = pg.G;
+    n.pa_perm = std::move(pg.perm);
+    n.pa_begins = std::move(pg.begins);
+    n.upk = std::move(pg.uniq);
+    ppks[ni].release();
+    if (n.children.empty() && n.P != G)
+      fail(FG_E_INTEGRITY, "relation " + n.name +
+                               ": leaf keys do not match its parent attributes");
   }
   tr.mark("parent grouping");
   // Edge lookups: own segment of i -> parent-key index of child c.
@@ -593,8 +609,6 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   }
   FG_CUDA(cudaEventRecord(ev.e[3], st));
   tr.mark("lookups+counts enqueue");
-  check_status(ctx, "compute_counts");
-  tr.mark("counts status sync");
 
   // ---- K3/K4/K5: the FiGaRo transform (figaro.hpp:166-329)
   for (auto it = preorder.rbegin(); it != preorder.rend(); ++it) {
@@ -821,9 +835,13 @@ void run(Context& ctx, int32_t n_rel, const fg_relation* rels, int32_t root,
   if (opt.memory == FG_MEM_HOST && N > 0)
     FG_CUDA(cudaMemcpyAsync(R_out, Rd, sizeof(double) * N * N,
                             cudaMemcpyDeviceToHost, st));
+  unsigned status_word = 0;
+  FG_CUDA(cudaMemcpyAsync(&status_word, ctx.status.get(), sizeof status_word,
+                          cudaMemcpyDeviceToHost, st));
   sync_stream(ctx);
   FG_CUDA(cudaGetLastError());
   tr.mark("final sync");
+  raise_status(status_word, "compute_counts");
 
   if (res) {
     res->data_columns = N;

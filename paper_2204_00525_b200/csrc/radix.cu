@@ -506,13 +506,19 @@ __global__ void __launch_bounds__(kSortThreads) k_segments(
     const KeyT* __restrict__ sorted, int64_t n, int* __restrict__ begins,
     uint64_t* __restrict__ uniq, int64_t* __restrict__ n_runs,
     const int* __restrict__ perm, int* __restrict__ pidx,
-    unsigned long long* __restrict__ look, uint32_t* __restrict__ ticket) {
+    unsigned long long* __restrict__ look, uint32_t* __restrict__ ticket,
+    const int64_t* __restrict__ n_dev) {
   __shared__ uint32_t s_tile, s_scan[kSortWarps], s_total;
   __shared__ unsigned long long s_pre;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // n_dev: the element count lives on the device (a group count not yet read
+  // by the host); the grid covers the host's upper bound and the tiles past
+  // the real end retire at once (nothing looks back at them).
+  if (n_dev) n = *n_dev;
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
+  if (tile * kSegTile >= n) return;
   const int64_t wbase = tile * kSegTile + (int64_t)warp * kSegIpt * 32;
   KeyT k[kSegIpt];
   uint32_t flags[kSegIpt];
@@ -731,7 +737,7 @@ void radix_sort_pairs(Context& ctx, const KeyT* keys_in, KeyT* keys_out, const i
 
 template <class KeyT>
 void launch_segments(Context& ctx, const KeyT* sorted, int64_t n, int* begins, uint64_t* uniq,
-                     int64_t* n_runs, const int* perm, int* pidx) {
+                     int64_t* n_runs, const int* perm, int* pidx, const int64_t* n_dev) {
   cudaStream_t st = ctx.stream;
   if (n == 0) {
     FG_CUDA(cudaMemsetAsync(n_runs, 0, sizeof(int64_t), st));
@@ -743,7 +749,7 @@ void launch_segments(Context& ctx, const KeyT* sorted, int64_t n, int* begins, u
   FG_CUDA(cudaMemsetAsync(look.get(), 0, look.bytes(), st));
   k_segments<KeyT><<<(unsigned)tiles, kSortThreads, 0, st>>>(
       sorted, n, begins, uniq, n_runs, perm, pidx, look.get() + 2,
-      reinterpret_cast<uint32_t*>(look.get()));
+      reinterpret_cast<uint32_t*>(look.get()), n_dev);
   FG_LAUNCHED(ctx);
   FG_KERNEL_CHECK();
 }
@@ -787,8 +793,8 @@ template void radix_sort_pairs<uint64_t>(Context&, const uint64_t*, uint64_t*, c
 template void radix_sort_pairs<uint32_t>(Context&, const uint32_t*, uint32_t*, const int*, int*,
                                          int64_t, int, const uint32_t*);
 template void launch_segments<uint64_t>(Context&, const uint64_t*, int64_t, int*, uint64_t*,
-                                        int64_t*, const int*, int*);
+                                        int64_t*, const int*, int*, const int64_t*);
 template void launch_segments<uint32_t>(Context&, const uint32_t*, int64_t, int*, uint64_t*,
-                                        int64_t*, const int*, int*);
+                                        int64_t*, const int*, int*, const int64_t*);
 
 }  // namespace fg
