@@ -190,20 +190,28 @@ __device__ __forceinline__ int64_t seg_of(const int* __restrict__ begins,
 
 struct NoFuse {};
 
-template <int CAP, int VJR = 1>
+// Row-groups work on contiguous chunks of a batch at the same time; with
+// power-of-two chunk strides their shared-memory reads fall on the same banks
+// (ncu on C3's width-8 own pass: 387 M of 835 M shared wavefronts were bank
+// conflicts).  The unfused kernels therefore index row metadata by
+// rr + rr / chunk (one padding entry per chunk) and shift the staged rows of
+// chunk g by g * px rows; kPadRows covers up to 8 row-groups (widths >= 8).
+constexpr int kPadRows = 8;
+template <int CAP, int VJR = 1, int PAD = 0>
 struct WarpSmemT {
+  static constexpr int kPad = PAD;
   double buf[CAP];
-  double2 coef[kMaxRB];   // {alpha, beta}: tail = a*alpha - S*beta
-  double hco[kMaxRB];     // head coefficient at a group's last row
-  double wt[kMaxRB];      // generalized weights (plain: the group's scale)
-  int2 segfl[kMaxRB];     // {group, flags}: bit0 start, bit1 last
+  double2 coef[kMaxRB + PAD];   // {alpha, beta}: tail = a*alpha - S*beta
+  double hco[kMaxRB + PAD];     // head coefficient at a group's last row
+  double wt[kMaxRB + PAD];      // generalized weights (plain: the group's scale)
+  int2 segfl[kMaxRB + PAD];     // {group, flags}: bit0 start, bit1 last
   unsigned char startf[kMaxRB];  // 1 where a group starts inside the batch
-  const double* rowptr[kMaxRB];  // staging: source row; afterwards: the row's tail slot (or null)
-  double* hrowp[kMaxRB];         // head row of a group's last row (or null)
+  const double* rowptr[kMaxRB + PAD];  // staging: source row; afterwards: the row's tail slot (or null)
+  double* hrowp[kMaxRB + PAD];         // head row of a group's last row (or null)
   double vjf[VJR][kVJMax + 1];   // join-on-read factors per staged row
   int vjidx[VJR][kVJMax];        // join-on-read child rows per staged row
 };
-using WarpSmem = WarpSmemT<kSmemDoubles>;
+using WarpSmem = WarpSmemT<kSmemDoubles, 1, kPadRows>;
 using WarpSmemVJ = WarpSmemT<kSmemDoubles, kVJRows>;
 constexpr int kFusedDoubles = 1280;  // one TSQR tile of tails (B x ls)
 
@@ -267,10 +275,13 @@ __device__ __forceinline__ void cp_async(double* dst, const double* src, bool na
 // pv (KP > 0): the batch's permutation entries, row lane + 32 k in pv[k],
 // loaded one batch ahead by the caller so the row gathers do not wait on a
 // dependent index load.
+// ch > 0: padded indexing (see kPadRows) with chunks of ch rows and a row
+// shift of px per chunk; ch = 0: plain indexing.
 template <int SLOTS, int VEC, bool VJ, class SM, class GEO, int KP = 0>
 __device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
                                            SM& sm, int64_t p, int nb,
-                                           int lane, const int* pv = nullptr) {
+                                           int lane, const int* pv = nullptr,
+                                           int ch = 0, int px = 0) {
   if constexpr (VJ) {
     // Join-on-read: own head columns and child summary rows are copied into
     // the row buffer; the row factors are applied when the buffer is read.
@@ -311,27 +322,43 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
       const int rr = lane + 32 * k;
       if (rr < nb) {
         const int64_t x = a.perm ? (int64_t)pv[k] : p + rr;
-        sm.rowptr[rr] = a.data + x * a.ld;
-        if (a.weights) sm.wt[rr] = a.weights[x];
+        const int m = ch ? rr + rr / ch : rr;
+        sm.rowptr[m] = a.data + x * a.ld;
+        if (a.weights) sm.wt[m] = a.weights[x];
       }
     }
   } else {
     for (int rr = lane; rr < nb; rr += 32) {
       const int64_t x = src_row(a, p + rr);
-      sm.rowptr[rr] = a.data + x * a.ld;
-      if (a.weights) sm.wt[rr] = a.weights[x];
+      const int m = ch ? rr + rr / ch : rr;
+      sm.rowptr[m] = a.data + x * a.ld;
+      if (a.weights) sm.wt[m] = a.weights[x];
     }
   }
   __syncwarp();
   const int g = lane / geo.L, cl = lane % geo.L;
   const bool narrow = a.perm != nullptr && a.w < 16 && a.l2hint;
-  for (int rr = g < geo.G ? g : nb; rr < nb; rr += geo.G) {
-    const double* src = sm.rowptr[rr];
-    double* dst = sm.buf + rr * geo.ls;
+  if (ch) {
+    // each row-group copies its own chunk (the rows it will scan)
+    const int r_lo = min(nb, g * ch), r_hi = g < geo.G ? min(nb, r_lo + ch) : r_lo;
+    for (int rr = r_lo; rr < r_hi; ++rr) {
+      const double* src = sm.rowptr[rr + g];
+      double* dst = sm.buf + (rr + g * px) * geo.ls;
 #pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int pk = cl + geo.L * s;
-      if (pk < geo.np) cp_async<VEC>(dst + VEC * pk, src + VEC * pk, narrow);
+      for (int s = 0; s < SLOTS; ++s) {
+        const int pk = cl + geo.L * s;
+        if (pk < geo.np) cp_async<VEC>(dst + VEC * pk, src + VEC * pk, narrow);
+      }
+    }
+  } else {
+    for (int rr = g < geo.G ? g : nb; rr < nb; rr += geo.G) {
+      const double* src = sm.rowptr[rr];
+      double* dst = sm.buf + rr * geo.ls;
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s) {
+        const int pk = cl + geo.L * s;
+        if (pk < geo.np) cp_async<VEC>(dst + VEC * pk, src + VEC * pk, narrow);
+      }
     }
   }
   __pipeline_commit();
@@ -437,7 +464,16 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
       tsv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? fast_sqrt_d((double)a.tail_count[gi]) : 1.0;
       hmv[k] = (a.head_mul && i <= nb && gi < a.n_seg) ? a.head_mul[gi] : 1.0;
     }
-    if (w > 0) stage_rows<SLOTS, VEC, VJ, SM, GEO, KP>(a, geo, sm, pb, nb, lane, pcur);
+    // Chunk of rows per row-group, and the padded indexing of the unfused
+    // kernels (kPadRows): metadata of row rr at rr + rr / ch, its staged data
+    // px rows further per chunk when the chunk stride would alias the banks.
+    const int ch = (nb + geo.G - 1) / geo.G;
+    const bool padded = !FUSED && !VJ && SM::kPad > 0 && geo.G > 1 && geo.G <= SM::kPad;
+    const int cap_rows = w > 0 ? kSmemDoubles / w : 0;
+    const int px = (padded && geo.L < 8 && (ch * w * 8) % 128 == 0 && nb + geo.G <= cap_rows) ? 1 : 0;
+    auto mi = [&](int rr) { return padded ? rr + rr / ch : rr; };
+    if (w > 0)
+      stage_rows<SLOTS, VEC, VJ, SM, GEO, KP>(a, geo, sm, pb, nb, lane, pcur, padded ? ch : 0, px);
     else if (VJ) __syncwarp();
     // Group starts inside the batch (groups g+1 .. g+nb can start here):
     // flagged in shared memory, then each row's group is g plus a ballot
@@ -502,7 +538,7 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
         jj = p - b0;
         m = b1 - b0;
         fl = (jj == 0 ? 1 : 0) | (p == b1 - 1 ? 2 : 0);
-        if (VJ || (weighted && w > 0)) v = sm.wt[rr];  // staged with the row (stage_rows)
+        if (VJ || (weighted && w > 0)) v = sm.wt[mi(rr)];  // staged with the row (stage_rows)
         else if (weighted) v = a.weights[src_row(a, p)];
       }
       double ts = 1.0;
@@ -571,16 +607,17 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
         N = __shfl_sync(0xffffffffu, incl, last_lane);
       }
       if (live) {
-        sm.coef[rr] = make_double2(al, be);
+        const int mx = mi(rr);
+        sm.coef[mx] = make_double2(al, be);
         // head_mul: the join's own-column factor prod_c s_c folded into the
         // head coefficient (figaro.hpp:226, `dst[j] *= all`)
-        sm.hco[rr] = hc * hmr;
-        sm.wt[rr] = weighted ? v : sc;  // plain rows never read their weight
-        sm.segfl[rr] = make_int2((int)sg, fl);
+        sm.hco[mx] = hc * hmr;
+        sm.wt[mx] = weighted ? v : sc;  // plain rows never read their weight
+        sm.segfl[mx] = make_int2((int)sg, fl);
         // Output rows of the emission pass, computed once per row here
         // instead of once per lane there (64-bit index arithmetic).
         const int64_t p = pb + rr;
-        sm.rowptr[rr] = (a.tails && !(fl & 1)) ? a.tails + (p - sg - 1) * a.ldt : nullptr;
+        sm.rowptr[mx] = (a.tails && !(fl & 1)) ? a.tails + (p - sg - 1) * a.ldt : nullptr;
         double* hp = nullptr;
         if (fl & 2) {
           const int64_t hi = a.head_index ? a.head_index[sg] : sg;
@@ -588,7 +625,7 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
           if (a.scales && a.wj < 0)
             a.scales[hi] = a.scale_count ? sqrt((double)a.scale_count[sg]) : sc;
         }
-        sm.hrowp[rr] = hp;
+        sm.hrowp[mx] = hp;
       }
     }
     if (w > 0) __pipeline_wait_prior(0);
@@ -596,8 +633,9 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
     if (w > 0) {
       // Rows of this batch are split into G contiguous chunks, one per
       // row-group.  Pass 1: chunk-local sums since the last group start.
-      const int ch = (nb + geo.G - 1) / geo.G;
       const int r_lo = min(nb, grp * ch), r_hi = min(nb, r_lo + ch);
+      // this row-group's offsets into the metadata arrays / the staged rows
+      const int mo = padded ? grp : 0, xo = grp * px;
       double loc[SLOTS][VEC];
 #pragma unroll
       for (int s = 0; s < SLOTS; ++s)
@@ -605,10 +643,10 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
         for (int e = 0; e < VEC; ++e) loc[s][e] = 0.0;
       int has_start = 0;
       for (int rr = r_lo; rr < r_hi; ++rr) {
-        const int fl = sm.segfl[rr].y;
-        const double vw = sm.wt[rr];
+        const int fl = sm.segfl[rr + mo].y;
+        const double vw = sm.wt[rr + mo];
         if (fl & 1) has_start = 1;
-        const double* row = sm.buf + rr * geo.ls;
+        const double* row = sm.buf + (rr + xo) * geo.ls;
 #pragma unroll
         for (int s = 0; s < SLOTS; ++s) {
           const int pk = cl + geo.L * s;
@@ -663,13 +701,13 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
         }
       // Pass 3: emit tails (and heads at group ends) for this chunk.
       for (int rr = r_lo; rr < r_hi; ++rr) {
-        const int2 sf = sm.segfl[rr];
-        const double2 cf = sm.coef[rr];
-        const double vw = sm.wt[rr];
-        double* trow = const_cast<double*>(sm.rowptr[rr]);
-        double* hrow = sm.hrowp[rr];
-        const double hc = hrow ? sm.hco[rr] : 0.0;
-        const double* row = sm.buf + rr * geo.ls;
+        const int2 sf = sm.segfl[rr + mo];
+        const double2 cf = sm.coef[rr + mo];
+        const double vw = sm.wt[rr + mo];
+        double* trow = const_cast<double*>(sm.rowptr[rr + mo]);
+        double* hrow = sm.hrowp[rr + mo];
+        const double hc = hrow ? sm.hco[rr + mo] : 0.0;
+        const double* row = sm.buf + (rr + xo) * geo.ls;
         // Join-on-write factors of this group (process_and_join_children,
         // figaro.hpp:196-230, in its product order).
         double jsc[kVJMax];
@@ -739,7 +777,7 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
         }
         if (jwrite) {
           // The children's summary columns of the joined row, and its scale.
-          const double sk = sm.wt[rr];  // plain transform: the group's scale
+          const double sk = sm.wt[rr + mo];  // plain transform: the group's scale
           for (int col = w + cl; col < a.wwidth; col += geo.L) {
             int c = 0;
             while (c + 1 < a.wj && col >= a.woff[c + 1]) ++c;
@@ -778,7 +816,7 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
         absorb_tile<F>(X, Racc, r, c, cols);
       }
     }
-    g = sm.segfl[nb - 1].x;
+    g = sm.segfl[mi(nb - 1)].x;
     __syncwarp();
   }
 }
@@ -1160,8 +1198,13 @@ __global__ void __launch_bounds__(kJoinTile) k_join_tile(const __grid_constant__
   __shared__ int is[kJoinTile][kJoinMaxC];
   const int nc = a.n_children;
   const int hw = (int)(a.width >> 1);
-  const int tr = threadIdx.x / hw, tp = threadIdx.x - (threadIdx.x / hw) * hw;
-  const int rpp = kJoinTile / hw;  // rows per pass (>= 1)
+  // Threads cover only the packets this kernel writes: with the own columns
+  // already final (own_done) a row's child packets alone, so every lane
+  // stores (C3: 6 of 10 packets per row).
+  const int pbase = a.own_done ? a.own_w >> 1 : 0;
+  const int pw = hw - pbase > 0 ? hw - pbase : 1;
+  const int tr = threadIdx.x / pw, tp = pbase + threadIdx.x - (threadIdx.x / pw) * pw;
+  const int rpp = kJoinTile / pw;  // rows per pass (>= 1)
   const int j = 2 * tp;
   int c = 0;
   if (j >= a.own_w)
@@ -1197,7 +1240,7 @@ __global__ void __launch_bounds__(kJoinTile) k_join_tile(const __grid_constant__
       }
     }
     __syncthreads();
-    if (tr < rpp) {
+    if (tr < rpp && j < a.width) {
 #pragma unroll kJoinUnroll
       for (int r = tr; r < rows; r += rpp) {
         double2* dst = reinterpret_cast<double2*>(a.S + (k0 + r) * a.width) + tp;

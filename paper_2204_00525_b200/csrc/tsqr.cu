@@ -326,7 +326,16 @@ using L32 = LCfg<32, 64, 2, 6, 1>;
 using L40 = LCfg<40, 64, 2, 6, 1>;
 using L48 = LCfg<48, 64, 2, 5, 1>;
 using L64 = LCfg<64, 64, 4, 3, 1>;
-using L64t = LCfg<64, 64, 2, 4, 1, 1>;
+#ifndef FG_L64T_B
+#define FG_L64T_B 64
+#endif
+#ifndef FG_L64T_MINB
+#define FG_L64T_MINB 4
+#endif
+#ifndef FG_L64T_WARPS
+#define FG_L64T_WARPS 2
+#endif
+using L64t = LCfg<64, FG_L64T_B, FG_L64T_WARPS, FG_L64T_MINB, 1, 1>;
 using L128 = LCfg<128, 64, 8, 1, 1>;
 using L128t = LCfg<128, 32, 4, 2, 1, 1>;
 
