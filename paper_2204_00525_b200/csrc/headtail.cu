@@ -454,14 +454,19 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
     // g+nb+1] and tail scales sqrt(tail_count[g .. g+nb]) are loaded now,
     // three per lane in registers, so their latency overlaps the row
     // gathers below instead of following them (read back by shuffles).
+    // (The counts stay raw here: converting them now would make the warp
+    // wait for these loads before it has issued the row gathers -- 44 % of
+    // the stall samples of C3's own pass; the square root is taken per row
+    // in the metadata pass.)
     int bgv[KS];
-    double tsv[KS], hmv[KS];
+    unsigned long long tcv[KS];
+    double hmv[KS];
 #pragma unroll
     for (int k = 0; k < KS; ++k) {
       const int i = lane + 32 * k;
       const int64_t gi = g + i;
       bgv[k] = (i <= nb + 1 && gi <= a.n_seg) ? a.begins[gi] : INT_MAX;
-      tsv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? fast_sqrt_d((double)a.tail_count[gi]) : 1.0;
+      tcv[k] = (a.tail_count && i <= nb && gi < a.n_seg) ? a.tail_count[gi] : 1ull;
       hmv[k] = (a.head_mul && i <= nb && gi < a.n_seg) ? a.head_mul[gi] : 1.0;
     }
     // Chunk of rows per row-group, and the padded indexing of the unfused
@@ -500,13 +505,13 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
       return v;
     };
     auto ts_at = [&](int i) -> double {
-      double v = __shfl_sync(0xffffffffu, tsv[0], i & 31);
+      unsigned long long v = __shfl_sync(0xffffffffu, tcv[0], i & 31);
 #pragma unroll
       for (int k = 1; k < KS; ++k) {
-        const double vk = __shfl_sync(0xffffffffu, tsv[k], i & 31);
+        const unsigned long long vk = __shfl_sync(0xffffffffu, tcv[k], i & 31);
         if ((i >> 5) == k) v = vk;
       }
-      return v;
+      return fast_sqrt_d((double)v);  // exact for perfect squares
     };
     auto hm_at = [&](int i) -> double {
       double v = __shfl_sync(0xffffffffu, hmv[0], i & 31);

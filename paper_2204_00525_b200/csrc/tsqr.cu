@@ -310,7 +310,16 @@ using W12c = WCfg<12, 3, 12, 2>;  // 96-row tiles (measured best at W = 12)
 using W16 = WCfg<16, 2, 8, 2>;
 using W16c = WCfg<16, 4, 8, 2>;
 using W20 = WCfg<20, 5, 8, 1>;
-using W20t = WCfg<20, 5, 14, 1>;  // 112-row tiles (measured best at W = 20)
+#ifndef FG_W20_RPT
+#define FG_W20_RPT 14
+#endif
+#ifndef FG_W20_MINB
+#define FG_W20_MINB 1
+#endif
+#ifndef FG_W20_WARPS
+#define FG_W20_WARPS 8
+#endif
+using W20t = WCfg<20, 5, FG_W20_RPT, FG_W20_MINB, 0, FG_W20_WARPS>;  // 112-row tiles (measured best at W = 20)
 using W24 = WCfg<24, 3, 8, 2>;
 using W32c = WCfg<32, 4, 8, 2>;
 using C16 = Cfg<16, 8, 16, 16>;
@@ -420,7 +429,7 @@ auto with_kernel(int W, Kern k, F&& f) {
 }
 
 template <class C> struct IsWarp : std::false_type {};
-template <int A, int B_, int C_, int D, int E> struct IsWarp<WCfg<A, B_, C_, D, E>> : std::true_type {};
+template <int A, int B_, int C_, int D, int E, int F_> struct IsWarp<WCfg<A, B_, C_, D, E, F_>> : std::true_type {};
 template <class C> struct IsLa : std::false_type {};
 template <int A, int B_, int C_, int D, int E, int G> struct IsLa<LCfg<A, B_, C_, D, E, G>> : std::true_type {};
 

@@ -93,7 +93,7 @@ __device__ __forceinline__ Reflector make_reflector_warp(double alpha, double si
 // ROLL_ = 1 keeps only the column-block loop unrolled in absorb_tile (the
 // TC steps inside a block run as a loop): ~1/TC of the code, for kernels
 // whose straight-line body overflows the instruction cache.
-template <int W_, int CPT_, int RPT_, int MINB_ = 1, int ROLL_ = 0>
+template <int W_, int CPT_, int RPT_, int MINB_ = 1, int ROLL_ = 0, int WARPS_ = 8>
 struct WCfg {
   static constexpr int W = W_;
   static constexpr int CPT = CPT_;
@@ -102,7 +102,7 @@ struct WCfg {
   static constexpr int RPT = RPT_;
   static constexpr int B = TR * RPT;
   static constexpr int RR = (W + TR - 1) / TR;  // accumulator rows per lane
-  static constexpr int WARPS = 8;
+  static constexpr int WARPS = WARPS_;
   static constexpr int NT = 32 * WARPS;
   static constexpr int MINB = MINB_;
   static constexpr int ROLL = ROLL_;
