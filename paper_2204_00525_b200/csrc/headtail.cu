@@ -89,6 +89,8 @@ struct HtDev {
   const int64_t* qb;     // per unit: its first row (n_units + 1 entries, or null)
   const double* head_mul;  // per group: heads *= head_mul[g] (or null)
   int l2hint;              // 1: L2::64B fetch hint for permuted short rows (cp_async)
+  int bulk_ok;             // 1: rows contiguous and 16-byte aligned: batches by one bulk copy
+  int rowbulk_ok;          // 1: rows 16-byte aligned and long enough: one bulk copy per row
   // Join-on-read (K4 folded into K5; process_and_join_children,
   // figaro.hpp:196-230): with nj >= 0 the data row x is never materialised;
   // it is [jhead[x, :own_w] * all | jS[c][jlidx[c][x]] * f_c ...] with
@@ -208,6 +210,7 @@ struct WarpSmemT {
   unsigned char startf[kMaxRB];  // 1 where a group starts inside the batch
   const double* rowptr[kMaxRB + PAD];  // staging: source row; afterwards: the row's tail slot (or null)
   double* hrowp[kMaxRB + PAD];         // head row of a group's last row (or null)
+  unsigned long long bar;              // mbarrier of the bulk-copied batches
   double vjf[VJR][kVJMax + 1];   // join-on-read factors per staged row
   int vjidx[VJR][kVJMax];        // join-on-read child rows per staged row
 };
@@ -271,6 +274,59 @@ __device__ __forceinline__ void cp_async(double* dst, const double* src, bool na
   }
 }
 
+// mbarrier + 1-D bulk copy (TMA engine, no tensor map) for batches whose rows
+// are contiguous in memory (project-away in identity order): one lane issues
+// one copy for the whole batch instead of every lane issuing LDGSTS packets,
+// which takes the staging off the LSU data pipe (18 % of its wavefronts on
+// C3's project-away, which runs that pipe at 86 %).
+__device__ __forceinline__ uint32_t ht_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ht_mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ht_smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void ht_bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+  // earlier generic-proxy reads of the buffer are ordered before the async write
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ht_smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(ht_smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(ht_smem_u32(bar))
+      : "memory");
+}
+// The same in two steps, for batches copied row by row: one lane announces
+// the batch's bytes, every lane copies the rows it owns.
+__device__ __forceinline__ void ht_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ht_smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void ht_bulk_row(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(ht_smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(ht_smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ht_mbar_wait(unsigned long long* bar, unsigned phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+        "p; }"
+        : "=r"(ok)
+        : "r"(ht_smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
 // Copies rows [p, p+nb) of the sorted order (w doubles each) into buf.
 // pv (KP > 0): the batch's permutation entries, row lane + 32 k in pv[k],
 // loaded one batch ahead by the caller so the row gathers do not wait on a
@@ -281,7 +337,7 @@ template <int SLOTS, int VEC, bool VJ, class SM, class GEO, int KP = 0>
 __device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
                                            SM& sm, int64_t p, int nb,
                                            int lane, const int* pv = nullptr,
-                                           int ch = 0, int px = 0) {
+                                           int ch = 0, int px = 0, int bulk = 0) {
   if constexpr (VJ) {
     // Join-on-read: own head columns and child summary rows are copied into
     // the row buffer; the row factors are applied when the buffer is read.
@@ -314,6 +370,37 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
       }
     }
     __pipeline_commit();
+    return;
+  }
+  if (bulk == 2) {
+    // one bulk copy per row, issued by the lane that owns the row
+    if (lane == 0) ht_expect_tx(&sm.bar, (unsigned)(nb * a.w * sizeof(double)));
+    const unsigned rbytes = (unsigned)(a.w * sizeof(double));
+    auto row_copy = [&](int rr, int64_t x) {
+      const int gq = ch ? rr / ch : 0;
+      ht_bulk_row(sm.buf + (rr + gq * px) * geo.ls, a.data + x * a.ld, rbytes, &sm.bar);
+      if (a.weights) sm.wt[rr + gq] = a.weights[x];
+    };
+    if constexpr (KP > 0) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int rr = lane + 32 * k;
+        if (rr < nb) row_copy(rr, a.perm ? (int64_t)pv[k] : p + rr);
+      }
+    } else {
+      for (int rr = lane; rr < nb; rr += 32) row_copy(rr, src_row(a, p + rr));
+    }
+    __syncwarp();
+    return;
+  }
+  if (bulk == 1) {
+    // contiguous rows (identity order, ld == w, px == 0): one bulk copy
+    if (lane == 0)
+      ht_bulk_g2s(sm.buf, a.data + p * a.ld, (unsigned)(nb * a.w * sizeof(double)), &sm.bar);
+    if (a.weights) {
+      for (int rr = lane; rr < nb; rr += 32) sm.wt[ch ? rr + rr / ch : rr] = a.weights[p + rr];
+    }
+    __syncwarp();
     return;
   }
   if constexpr (KP > 0) {
@@ -370,7 +457,7 @@ __device__ __forceinline__ void stage_rows(const HtDev& a, const GEO& geo,
 template <int SLOTS, int VEC, class F, bool VJ, class SM, class RA, bool JW = false,
           class GEO = Geo>
 __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
-                             int64_t u, int lane, RA& Racc) {
+                             int64_t u, int lane, RA& Racc, unsigned& bphase) {
   constexpr bool FUSED = !std::is_same<F, NoFuse>::value;
   constexpr int CW = GeoW<GEO>::value;
   const int w = CW ? CW : a.w;
@@ -477,8 +564,13 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
     const int cap_rows = w > 0 ? kSmemDoubles / w : 0;
     const int px = (padded && geo.L < 8 && (ch * w * 8) % 128 == 0 && nb + geo.G <= cap_rows) ? 1 : 0;
     auto mi = [&](int rr) { return padded ? rr + rr / ch : rr; };
+    const int bulk = (FUSED || VJ || w <= 0) ? 0
+                     : (a.bulk_ok && px == 0)   ? 1
+                     : a.rowbulk_ok             ? 2
+                                                : 0;
     if (w > 0)
-      stage_rows<SLOTS, VEC, VJ, SM, GEO, KP>(a, geo, sm, pb, nb, lane, pcur, padded ? ch : 0, px);
+      stage_rows<SLOTS, VEC, VJ, SM, GEO, KP>(a, geo, sm, pb, nb, lane, pcur, padded ? ch : 0, px,
+                                              bulk);
     else if (VJ) __syncwarp();
     // Group starts inside the batch (groups g+1 .. g+nb can start here):
     // flagged in shared memory, then each row's group is g plus a ballot
@@ -633,7 +725,12 @@ __device__ void process_unit(const HtDev& a, const GEO& geo, SM& sm,
         sm.hrowp[mx] = hp;
       }
     }
-    if (w > 0) __pipeline_wait_prior(0);
+    if (bulk) {
+      ht_mbar_wait(&sm.bar, bphase);
+      bphase ^= 1u;
+    } else if (w > 0) {
+      __pipeline_wait_prior(0);
+    }
     __syncwarp();
     if (w > 0) {
       // Rows of this batch are split into G contiguous chunks, one per
@@ -836,6 +933,9 @@ __global__ void __launch_bounds__(kWarps * 32, (VJ || JW || SLOTS > 1) ? 1 : FG_
   const int lane = threadIdx.x & 31;
   SMT& sm = all[warp];
   int dummy = 0;
+  unsigned bphase = 0;
+  if (lane == 0) ht_mbar_init(&sm.bar);
+  __syncwarp();
   while (true) {
     int64_t u = 0;
     if (lane == 0) u = atomicAdd(a.ticket, 1);
@@ -843,9 +943,9 @@ __global__ void __launch_bounds__(kWarps * 32, (VJ || JW || SLOTS > 1) ? 1 : FG_
     if (u >= a.n_units) break;
     if constexpr (CW > 0) {
       const GeoC<CW> gc{};
-      process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW, GeoC<CW>>(a, gc, sm, u, lane, dummy);
+      process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW, GeoC<CW>>(a, gc, sm, u, lane, dummy, bphase);
     } else {
-      process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW>(a, geo, sm, u, lane, dummy);
+      process_unit<SLOTS, VEC, NoFuse, VJ, SMT, int, JW>(a, geo, sm, u, lane, dummy, bphase);
     }
   }
 }
@@ -869,9 +969,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, F::MINB)
     for (int q = 0; q < F::CPT; ++q) Racc[m][q] = 0.0;
   // Static unit -> warp assignment: which rows each accumulator absorbs
   // (and so the rounding of R) depends only on the grid, not on timing.
+  unsigned bphase_unused = 0;
   const int64_t nw = (int64_t)gridDim.x * kFusedWarps;
   for (int64_t u = (int64_t)blockIdx.x * kFusedWarps + warp; u < a.n_units; u += nw)
-    process_unit<1, VEC, F, false>(a, geo, sm, u, lane, Racc);
+    process_unit<1, VEC, F, false>(a, geo, sm, u, lane, Racc, bphase_unused);
   const int r = lane % F::TR, c = lane / F::TR;
   double* o = partials + ((int64_t)blockIdx.x * kFusedWarps + warp) * F::W * F::W;
 #pragma unroll
@@ -1376,6 +1477,18 @@ static void prepare(Context& ctx, const HeadTailArgs& in, HtPrep& P, int rb_fixe
   d.scales = in.scales;
   d.head_mul = in.head_mul;
   d.l2hint = getenv("FG_NO_L2_HINT") == nullptr;
+  d.bulk_ok = !in.perm && !in.join && !in.join_write && in.w > 0 && in.ld == in.w &&
+              in.w % 2 == 0 && reinterpret_cast<uintptr_t>(in.data) % 16 == 0 &&
+              getenv("FG_NO_BULK") == nullptr;
+  {
+    // Per-row bulk copies for rows of at least FG_ROW_BULK_MIN doubles
+    // (default 16: a 128-byte line) that start on 16-byte boundaries.
+    const char* e = getenv("FG_ROW_BULK_MIN");
+    const int min_w = e ? atoi(e) : 16;
+    d.rowbulk_ok = !in.join && !in.join_write && in.w >= min_w && in.w % 2 == 0 &&
+                   in.ld % 2 == 0 && reinterpret_cast<uintptr_t>(in.data) % 16 == 0 &&
+                   getenv("FG_NO_BULK") == nullptr;
+  }
   d.nj = -1;
   d.wj = -1;
   if (in.join_write) {
