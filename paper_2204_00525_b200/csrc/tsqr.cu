@@ -233,10 +233,44 @@ __global__ void __launch_bounds__(C::NT)
 // whole column loop is straight-line register code: pivot broadcast by
 // shuffle, reflector computed redundantly by every lane (branch-free, tau = 0
 // for an all-zero column), dot products reduced over the TR row lanes.
-template <class C>
+// bulk = 1 (one dense span of exactly W columns, 16-byte aligned): a warp's
+// next tile is fetched by one 1-D bulk copy (TMA engine) into its shared-
+// memory slot while the current tile is absorbed -- the slot is free as soon
+// as the tile sits in registers -- instead of 8-byte loads whose latency the
+// 8 resident warps cannot hide (10 % of the W = 20 kernel's stall samples).
+__device__ __forceinline__ uint32_t tw_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tw_bulk_tile(void* dst, const void* src, unsigned bytes,
+                                             unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tw_smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(tw_smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tw_smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tw_mbar_wait(unsigned long long* bar, unsigned phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+        "p; }"
+        : "=r"(ok)
+        : "r"(tw_smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
+template <class C, bool BULK>
 __global__ void __launch_bounds__(C::NT, C::MINB)
     k_tsqr_warp(const SegDev* __restrict__ segs, int nseg, int64_t total_rows,
                 int64_t total_tiles, int64_t nunits, double* __restrict__ out) {
+  constexpr bool bulk = BULK;
+  extern __shared__ __align__(16) unsigned char tw_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int r = lane % C::TR;
@@ -252,8 +286,40 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #pragma unroll
     for (int q = 0; q < C::CPT; ++q) Racc[m][q] = 0.0;
 
+  constexpr unsigned kTileBytes = C::B * C::W * sizeof(double);
+  double* tbuf = reinterpret_cast<double*>(tw_raw) + (size_t)wib * C::B * C::W;
+  unsigned long long* bar =
+      reinterpret_cast<unsigned long long*>(tw_raw + (size_t)C::WARPS * kTileBytes) + wib;
+  unsigned phase = 0;
+  const double* dense = nullptr;
+  if constexpr (bulk) {
+    dense = segs[0].data;
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tw_smem_u32(bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if ((gw + 1) * C::B <= total_rows)
+        tw_bulk_tile(tbuf, dense + gw * (int64_t)C::B * C::W, kTileBytes, bar);
+    }
+    __syncwarp();
+  }
+
   for (int64_t t = gw; t < total_tiles; t += nunits) {
     double X[C::RPT][C::CPT];
+    if (bulk && (t + 1) * C::B <= total_rows) {  // (compile-time false without BULK)
+      // full tiles arrive through the warp's slot (issued one tile ahead)
+      tw_mbar_wait(bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int i = 0; i < C::RPT; ++i)
+#pragma unroll
+        for (int q = 0; q < C::CPT; ++q) X[i][q] = tbuf[(i * C::TR + r) * C::W + cols[q]];
+      __syncwarp();
+      const int64_t tn = t + nunits;
+      if (lane == 0 && tn < total_tiles && (tn + 1) * C::B <= total_rows)
+        tw_bulk_tile(tbuf, dense + tn * (int64_t)C::B * C::W, kTileBytes, bar);
+      absorb_tile<C>(X, Racc, r, c, cols);
+      continue;
+    }
 #pragma unroll
     for (int i = 0; i < C::RPT; ++i) {
       const int64_t gr = t * C::B + i * C::TR + r;
@@ -404,9 +470,20 @@ template <class C>
 Plan plan_la(Context& ctx) {
   return {C::B, 1, resident(ctx, k_tsqr_la<C, SegDev>, C::NT, C::smem_bytes)};
 }
+// Shared memory of the warp kernel's bulk-copied tiles (one slot + one
+// mbarrier per warp), or 0 when MINB CTAs of it would not fit an SM.
 template <class C>
-Plan plan_warp(Context& ctx) {
-  return {C::B, C::WARPS, resident(ctx, k_tsqr_warp<C>, C::NT, C::smem_bytes)};
+size_t warp_bulk_smem(Context& ctx) {
+  const size_t need = (size_t)C::WARPS * (C::B * C::W * sizeof(double) + 8);
+  if (getenv("FG_TSQR_NO_BULK")) return 0;
+  return (need + 1024) * C::MINB <= 228u * 1024 && need <= ctx.smem_optin ? need : 0;
+}
+template <class C>
+Plan plan_warp(Context& ctx, bool bulk) {
+  const size_t smem = bulk ? warp_bulk_smem<C>(ctx) : 0;
+  return {C::B, C::WARPS,
+          smem ? resident(ctx, k_tsqr_warp<C, true>, C::NT, smem)
+               : resident(ctx, k_tsqr_warp<C, false>, C::NT, 0)};
 }
 
 // Runs `f` with the config type of width W / kernel k (unsupported
@@ -433,22 +510,27 @@ template <int A, int B_, int C_, int D, int E, int F_> struct IsWarp<WCfg<A, B_,
 template <class C> struct IsLa : std::false_type {};
 template <int A, int B_, int C_, int D, int E, int G> struct IsLa<LCfg<A, B_, C_, D, E, G>> : std::true_type {};
 
-Plan plan_for(Context& ctx, int W, int64_t rows) {
+Plan plan_for(Context& ctx, int W, int64_t rows, bool bulk) {
   return with_kernel(W, variant(W, rows), [&](auto cfg) -> Plan {
     using C = decltype(cfg);
-    if constexpr (IsWarp<C>::value) return plan_warp<C>(ctx);
+    if constexpr (IsWarp<C>::value) return plan_warp<C>(ctx, bulk);
     else if constexpr (IsLa<C>::value) return plan_la<C>(ctx);
     else return plan_cta<C>(ctx);
   });
 }
 
 void launch_for(Context& ctx, int W, const SegDev* segs, int nseg,
-                int64_t rows, int64_t tiles, int64_t units, int grid, double* out) {
+                int64_t rows, int64_t tiles, int64_t units, int grid, double* out, bool bulk) {
   cudaStream_t s = ctx.stream;
   with_kernel(W, variant(W, rows), [&](auto cfg) {
     using C = decltype(cfg);
-    if constexpr (IsWarp<C>::value)
-      k_tsqr_warp<C><<<grid, C::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+    if constexpr (IsWarp<C>::value) {
+      const size_t smem = bulk ? warp_bulk_smem<C>(ctx) : 0;
+      if (smem)
+        k_tsqr_warp<C, true><<<grid, C::NT, smem, s>>>(segs, nseg, rows, tiles, units, out);
+      else
+        k_tsqr_warp<C, false><<<grid, C::NT, 0, s>>>(segs, nseg, rows, tiles, units, out);
+    }
     else if constexpr (IsLa<C>::value)
       k_tsqr_la<C, SegDev><<<grid, C::NT, C::smem_bytes, s>>>(segs, nseg, rows, tiles, units, out);
     else
@@ -475,7 +557,16 @@ int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_unit
            DevArray<double>& out) {
   int64_t all_rows = 0;
   for (auto& s : segs) all_rows += s.rows;
-  const Plan p = plan_for(ctx, W, all_rows);
+  // One dense span of exactly W columns on 16-byte boundaries: the warp
+  // kernels fetch its tiles by bulk copies.
+  static const int64_t bulk_min_rows = [] {
+    const char* e = getenv("FG_TSQR_BULK_MIN_ROWS");
+    return e ? (int64_t)atoll(e) : (int64_t)1 << 20;
+  }();
+  const bool bulk = segs.size() == 1 && segs[0].cols == W && segs[0].ld == W &&
+                    segs[0].col_begin == 0 && (W % 2) == 0 && all_rows >= bulk_min_rows &&
+                    reinterpret_cast<uintptr_t>(segs[0].data) % 16 == 0;
+  const Plan p = plan_for(ctx, W, all_rows, bulk);
   // A unit must absorb more rows than a factor has, or merges cannot shrink.
   tiles_per_unit = std::max<int64_t>(tiles_per_unit, 2 * ceil_div(W, p.B));
   int64_t rows = 0;
@@ -491,7 +582,7 @@ int factor(Context& ctx, int W, std::vector<SegDev> segs, int64_t tiles_per_unit
   FG_CUDA(cudaMemcpyAsync(dsegs.get(), segs.data(), segs.size() * sizeof(SegDev),
                           cudaMemcpyHostToDevice, ctx.stream));
   out.alloc((size_t)units * W * W, ctx.stream);
-  launch_for(ctx, W, dsegs.get(), (int)segs.size(), rows, tiles, units, grid, out.get());
+  launch_for(ctx, W, dsegs.get(), (int)segs.size(), rows, tiles, units, grid, out.get(), bulk);
   // Pageable host -> device copies are staged before cudaMemcpyAsync
   // returns, so `segs` may go out of scope.  Every unit gets >= 1 tile.
   return (int)units;
